@@ -1,0 +1,410 @@
+/*
+ * o3g_oracle.c — CPU ORACLE for the point-to-plane ICP iteration.
+ *
+ * TEST INFRASTRUCTURE ONLY. Nothing on the product path may link, load or
+ * call this file: only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference legs use it. It shares no code, header,
+ * constant or helper with the CUDA library (paper_1801_09847_b200/csrc).
+ *
+ * Plain, slow, obviously-correct C99, compiled with
+ *   -O2 -ffp-contract=off -fno-fast-math   (SSE2 fp64, no FMA contraction)
+ * so every floating-point operation below is one IEEE-754 binary64
+ * operation in the order written.
+ *
+ * What it computes (citations: P:n = PAPER.md line n, S:n = SPEC.md line n,
+ * R#n = reading n of DESIGN.md §3 "Readings of the paper"):
+ *   - registration_icp(..., TransformationEstimationPointToPlane())
+ *     P:203-212 (§3.3), loop semantics S:282-290, refs [2],[4] P:267,P:269.
+ *   - Gauss-Newton step x <- x - (J^T J)^{-1} J^T r, Eq. 2, with
+ *     J^T J and J^T r summed over the data records.
+ *   - nearest neighbour within max_correspondence_distance,
+ *     inclusive d <= dmax, ties -> lower target index (R#1-R#3).
+ *   - fitness = inliers/|source|, inlier_rmse over the
+ *     correspondences (R#7).
+ *   - LDLT without pivoting + singularity guard (R#6).
+ *   - SE(3) exponential, twist (omega, v) rotation first, series for
+ *     |omega| < 1e-6 (R#5).
+ *   - convergence |dfit| < relative_fitness and |drmse| < relative_rmse
+ *     between consecutive passes (R#8: parity unpinned by paper).
+ *
+ * Correspondence search has two forms:
+ *   - brute force over every target point: the DEFINITION;
+ *   - a grid accelerator (cells of size dmax*(1+2^-24), 27-cell scan) that
+ *     tests/test_oracle.py checks equal to brute force.
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#if defined(__FP_FAST_FMA) && !defined(O3G_ORACLE_ALLOW_FMA)
+/* -ffp-contract=off is what matters; __FP_FAST_FMA only says FMA exists. */
+#endif
+
+/* ------------------------------------------------------------------ A3 */
+/* s' = T s with the fixed order ((T00 sx + T01 sy) + T02 sz) + T03
+ * (R#2), sx = (double) of the fp32 input. T is row-major 4x4.           */
+void orc_transform_point(const double T[16], const float p[3], double out[3])
+{
+    const double x = (double)p[0], y = (double)p[1], z = (double)p[2];
+    for (int r = 0; r < 3; ++r) {
+        double a = T[4 * r + 0] * x;
+        double b = T[4 * r + 1] * y;
+        double c = T[4 * r + 2] * z;
+        out[r] = ((a + b) + c) + T[4 * r + 3];
+    }
+}
+
+void orc_transform(const double T[16], const float *p, int64_t n, double *out)
+{
+    for (int64_t i = 0; i < n; ++i) orc_transform_point(T, p + 3 * i, out + 3 * i);
+}
+
+/* ------------------------------------------------------------------ A4 */
+/* d^2 = ((dx*dx + dy*dy) + dz*dz), dx = s'x - (double)qx (R#2).          */
+static double dist2(const double s[3], const float *q)
+{
+    double dx = s[0] - (double)q[0];
+    double dy = s[1] - (double)q[1];
+    double dz = s[2] - (double)q[2];
+    double xx = dx * dx, yy = dy * dy, zz = dz * dz;
+    return (xx + yy) + zz;
+}
+
+/* Keep j if d2 <= r2 (inclusive, R#1); the winner is the minimum d2 and,
+ * among equal d2, the lowest target index (R#3).                        */
+static int better(double d2, int64_t j, double best_d2, int64_t best_j)
+{
+    if (best_j < 0) return 1;
+    if (d2 < best_d2) return 1;
+    if (d2 == best_d2 && j < best_j) return 1;
+    return 0;
+}
+
+/* Brute force: the definition. Returns the index or -1.                 */
+int64_t orc_nn_brute(const double s[3], const float *tgt, int64_t m, double r2, double *d2_out)
+{
+    int64_t best = -1;
+    double bd = 0.0;
+    for (int64_t j = 0; j < m; ++j) {
+        double d2 = dist2(s, tgt + 3 * j);
+        if (d2 <= r2 && better(d2, j, bd, best)) { best = j; bd = d2; }
+    }
+    if (d2_out) *d2_out = bd;
+    return best;
+}
+
+/* ---------------------------------------------------------- grid (accel) */
+typedef struct { int64_t cz, cy, cx; int64_t idx; } orc_cellpt;
+
+typedef struct {
+    const float *tgt;
+    int64_t m;
+    double o[3];     /* componentwise min of the target */
+    double h;        /* cell size dmax*(1+2^-24) */
+    orc_cellpt *pts; /* sorted by (cz, cy, cx, idx) */
+} orc_grid;
+
+static int cmp_cellpt(const void *a_, const void *b_)
+{
+    const orc_cellpt *a = (const orc_cellpt *)a_, *b = (const orc_cellpt *)b_;
+    if (a->cz != b->cz) return a->cz < b->cz ? -1 : 1;
+    if (a->cy != b->cy) return a->cy < b->cy ? -1 : 1;
+    if (a->cx != b->cx) return a->cx < b->cx ? -1 : 1;
+    if (a->idx != b->idx) return a->idx < b->idx ? -1 : 1;
+    return 0;
+}
+
+static int64_t cell_coord(double x, double o, double h)
+{
+    double c = floor((x - o) / h);
+    if (c < -1099511627776.0) c = -1099511627776.0; /* clamp far queries: 2^40 */
+    if (c > 1099511627776.0) c = 1099511627776.0;
+    return (int64_t)c;
+}
+
+orc_grid *orc_grid_build(const float *tgt, int64_t m, double dmax)
+{
+    orc_grid *g = (orc_grid *)calloc(1, sizeof(orc_grid));
+    if (!g) return NULL;
+    g->tgt = tgt;
+    g->m = m;
+    g->h = dmax * (1.0 + 5.9604644775390625e-08); /* 2^-24 margin */
+    for (int a = 0; a < 3; ++a) g->o[a] = INFINITY;
+    for (int64_t j = 0; j < m; ++j)
+        for (int a = 0; a < 3; ++a)
+            if ((double)tgt[3 * j + a] < g->o[a]) g->o[a] = (double)tgt[3 * j + a];
+    g->pts = (orc_cellpt *)malloc(sizeof(orc_cellpt) * (size_t)(m > 0 ? m : 1));
+    if (!g->pts) { free(g); return NULL; }
+    for (int64_t j = 0; j < m; ++j) {
+        g->pts[j].cx = cell_coord((double)tgt[3 * j + 0], g->o[0], g->h);
+        g->pts[j].cy = cell_coord((double)tgt[3 * j + 1], g->o[1], g->h);
+        g->pts[j].cz = cell_coord((double)tgt[3 * j + 2], g->o[2], g->h);
+        g->pts[j].idx = j;
+    }
+    qsort(g->pts, (size_t)m, sizeof(orc_cellpt), cmp_cellpt);
+    return g;
+}
+
+void orc_grid_free(orc_grid *g)
+{
+    if (g) { free(g->pts); free(g); }
+}
+
+/* first position whose (cz,cy,cx) >= key (idx ignored) */
+static int64_t lower(const orc_grid *g, int64_t cz, int64_t cy, int64_t cx)
+{
+    int64_t lo = 0, hi = g->m;
+    orc_cellpt key = {cz, cy, cx, -1};
+    while (lo < hi) {
+        int64_t mid = lo + (hi - lo) / 2;
+        if (cmp_cellpt(&g->pts[mid], &key) < 0) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+
+int64_t orc_nn_grid(const orc_grid *g, const double s[3], double r2, double *d2_out)
+{
+    int64_t cx = cell_coord(s[0], g->o[0], g->h);
+    int64_t cy = cell_coord(s[1], g->o[1], g->h);
+    int64_t cz = cell_coord(s[2], g->o[2], g->h);
+    int64_t best = -1;
+    double bd = 0.0;
+    for (int64_t dz = -1; dz <= 1; ++dz)
+        for (int64_t dy = -1; dy <= 1; ++dy)
+            for (int64_t dx = -1; dx <= 1; ++dx) {
+                int64_t k = lower(g, cz + dz, cy + dy, cx + dx);
+                for (; k < g->m; ++k) {
+                    const orc_cellpt *c = &g->pts[k];
+                    if (c->cz != cz + dz || c->cy != cy + dy || c->cx != cx + dx) break;
+                    double d2 = dist2(s, g->tgt + 3 * c->idx);
+                    if (d2 <= r2 && better(d2, c->idx, bd, best)) { best = c->idx; bd = d2; }
+                }
+            }
+    if (d2_out) *d2_out = bd;
+    return best;
+}
+
+/* ------------------------------------------------------------ A5 / A6 */
+/* Neumaier-compensated accumulator, plus the sum of |terms| used by the
+ * reduction tolerance (R#14).                                           */
+typedef struct { double s, c, a; } acc_t;
+
+static void acc_add(acc_t *x, double v)
+{
+    double t = x->s + v;
+    if (fabs(x->s) >= fabs(v)) x->c += (x->s - t) + v;
+    else x->c += (v - t) + x->s;
+    x->s = t;
+    x->a += fabs(v);
+}
+
+/* 29 terms: JTJ upper triangle row-major (i<=j, 21), JTr (6), count, sum d^2 */
+enum { ORC_NTERMS = 29 };
+
+/* One correspondence record: r = (s'-q).n, J = [s' x n ; n] (R#4).       */
+static void record(const double s[3], const float *qf, const float *nf, double d2, acc_t acc[ORC_NTERMS])
+{
+    double q[3] = {(double)qf[0], (double)qf[1], (double)qf[2]};
+    double n[3] = {(double)nf[0], (double)nf[1], (double)nf[2]};
+    double r = ((s[0] - q[0]) * n[0] + (s[1] - q[1]) * n[1]) + (s[2] - q[2]) * n[2];
+    double J[6];
+    J[0] = s[1] * n[2] - s[2] * n[1];
+    J[1] = s[2] * n[0] - s[0] * n[2];
+    J[2] = s[0] * n[1] - s[1] * n[0];
+    J[3] = n[0];
+    J[4] = n[1];
+    J[5] = n[2];
+    int k = 0;
+    for (int i = 0; i < 6; ++i)
+        for (int j = i; j < 6; ++j) acc_add(&acc[k++], J[i] * J[j]);
+    for (int i = 0; i < 6; ++i) acc_add(&acc[21 + i], J[i] * r);
+    acc_add(&acc[27], 1.0);
+    acc_add(&acc[28], d2);
+}
+
+/* One pass at fixed T over source indices idx[0..k) (idx NULL -> 0..n).
+ * corr[t] gets the target index of idx[t] (or -1); d2out likewise.
+ * sums/abssums: the 29 terms and their sums of |term|.                  */
+void orc_pass_subset(const double T[16], const float *src, int64_t n, const int64_t *idx, int64_t k,
+                     const float *tgt, const float *nrm, int64_t m, const orc_grid *g, double dmax,
+                     int32_t *corr, double *d2out, double *sums, double *abssums)
+{
+    acc_t acc[ORC_NTERMS];
+    memset(acc, 0, sizeof(acc));
+    const double r2 = dmax * dmax;
+    int64_t cnt = idx ? k : n;
+    for (int64_t t = 0; t < cnt; ++t) {
+        int64_t i = idx ? idx[t] : t;
+        double s[3], d2 = 0.0;
+        orc_transform_point(T, src + 3 * i, s);
+        int64_t j = g ? orc_nn_grid(g, s, r2, &d2) : orc_nn_brute(s, tgt, m, r2, &d2);
+        if (corr) corr[t] = (int32_t)j;
+        if (d2out) d2out[t] = j >= 0 ? d2 : -1.0;
+        if (j >= 0) record(s, tgt + 3 * j, nrm + 3 * j, d2, acc);
+    }
+    for (int t = 0; t < ORC_NTERMS; ++t) {
+        if (sums) sums[t] = acc[t].s + acc[t].c;
+        if (abssums) abssums[t] = acc[t].a;
+    }
+}
+
+void orc_pass(const double T[16], const float *src, int64_t n, const float *tgt, const float *nrm,
+              int64_t m, const orc_grid *g, double dmax, int32_t *corr, double *sums, double *abssums)
+{
+    orc_pass_subset(T, src, n, NULL, 0, tgt, nrm, m, g, dmax, corr, NULL, sums, abssums);
+}
+
+/* ------------------------------------------------------------------ A8 */
+/* Full symmetric 6x6 from the 21 upper-triangle terms.                  */
+void orc_expand_jtj(const double *terms, double A[36])
+{
+    int k = 0;
+    for (int i = 0; i < 6; ++i)
+        for (int j = i; j < 6; ++j) { A[6 * i + j] = terms[k]; A[6 * j + i] = terms[k]; ++k; }
+}
+
+/* LDL^T without pivoting (R#6). Returns 0 on success, 1 if singular:
+ * some D_k <= 1e-12 * max_i A_ii (or max_i A_ii <= 0).                  */
+int orc_ldlt_solve(const double A[36], const double b[6], double x[6])
+{
+    double L[36] = {0}, D[6], y[6];
+    double dmax = 0.0;
+    for (int i = 0; i < 6; ++i) if (A[7 * i] > dmax) dmax = A[7 * i];
+    if (!(dmax > 0.0)) return 1;
+    for (int j = 0; j < 6; ++j) {
+        double d = A[6 * j + j];
+        for (int k = 0; k < j; ++k) d -= L[6 * j + k] * L[6 * j + k] * D[k];
+        if (!(d > 1e-12 * dmax)) return 1;
+        D[j] = d;
+        L[6 * j + j] = 1.0;
+        for (int i = j + 1; i < 6; ++i) {
+            double v = A[6 * i + j];
+            for (int k = 0; k < j; ++k) v -= L[6 * i + k] * L[6 * j + k] * D[k];
+            L[6 * i + j] = v / d;
+        }
+    }
+    for (int i = 0; i < 6; ++i) {            /* L y = b */
+        double v = b[i];
+        for (int k = 0; k < i; ++k) v -= L[6 * i + k] * y[k];
+        y[i] = v;
+    }
+    for (int i = 0; i < 6; ++i) y[i] /= D[i]; /* D z = y */
+    for (int i = 5; i >= 0; --i) {           /* L^T x = z */
+        double v = y[i];
+        for (int k = i + 1; k < 6; ++k) v -= L[6 * k + i] * x[k];
+        x[i] = v;
+    }
+    return 0;
+}
+
+/* SE(3) exponential of xi = (omega, v) (R#5):
+ *   R = I + A W + B W^2,  V = I + B W + C W^2,  t = V v,
+ *   A = sin(th)/th, B = (1-cos th)/th^2, C = (th - sin th)/th^3,
+ *   series 1 - th^2/6, 1/2 - th^2/24, 1/6 - th^2/120 for th < 1e-6.      */
+void orc_exp_se3(const double xi[6], double T[16])
+{
+    const double w[3] = {xi[0], xi[1], xi[2]}, v[3] = {xi[3], xi[4], xi[5]};
+    double th2 = w[0] * w[0] + w[1] * w[1] + w[2] * w[2];
+    double th = sqrt(th2), A, B, C;
+    if (th < 1e-6) {
+        A = 1.0 - th2 / 6.0;
+        B = 0.5 - th2 / 24.0;
+        C = 1.0 / 6.0 - th2 / 120.0;
+    } else {
+        A = sin(th) / th;
+        B = (1.0 - cos(th)) / th2;
+        C = (th - sin(th)) / (th2 * th);
+    }
+    double W[9] = {0, -w[2], w[1], w[2], 0, -w[0], -w[1], w[0], 0};
+    double W2[9];
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) {
+            double s = 0.0;
+            for (int k = 0; k < 3; ++k) s += W[3 * i + k] * W[3 * k + j];
+            W2[3 * i + j] = s;
+        }
+    double R[9], V[9];
+    for (int i = 0; i < 9; ++i) {
+        double I = (i % 4 == 0) ? 1.0 : 0.0;
+        R[i] = I + A * W[i] + B * W2[i];
+        V[i] = I + B * W[i] + C * W2[i];
+    }
+    memset(T, 0, 16 * sizeof(double));
+    for (int i = 0; i < 3; ++i) {
+        for (int j = 0; j < 3; ++j) T[4 * i + j] = R[3 * i + j];
+        T[4 * i + 3] = V[3 * i + 0] * v[0] + V[3 * i + 1] * v[1] + V[3 * i + 2] * v[2];
+    }
+    T[15] = 1.0;
+}
+
+/* C = A B for 4x4 row-major rigid transforms; bottom row set exactly.   */
+void orc_compose(const double A[16], const double B[16], double C[16])
+{
+    double out[16];
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 4; ++j) {
+            double s = 0.0;
+            for (int k = 0; k < 4; ++k) s += A[4 * i + k] * B[4 * k + j];
+            out[4 * i + j] = s;
+        }
+    out[12] = 0.0; out[13] = 0.0; out[14] = 0.0; out[15] = 1.0;
+    memcpy(C, out, sizeof(out));
+}
+
+/* ------------------------------------------------------------ the loop */
+enum { ORC_FLAG_NO_CORR = 1, ORC_FLAG_DEGENERATE = 2 };
+
+/* registration_icp, point-to-plane.
+ * max_iterations counts updates; passes = updates + 1. Returns fitness and
+ * rmse of the last pass, i.e. at the returned T. hist_* (nullable) get one
+ * entry per pass (max_iterations + 1 capacity).                         */
+int orc_icp(const float *src, int64_t n, const float *tgt, const float *nrm, int64_t m,
+            const double T0[16], double dmax, int32_t max_iterations, double relative_fitness,
+            double relative_rmse, int32_t use_grid, double T_out[16], double *fitness,
+            double *inlier_rmse, int32_t *iterations, int32_t *flags, int32_t *converged,
+            double *hist_fit, double *hist_rmse)
+{
+    orc_grid *g = use_grid ? orc_grid_build(tgt, m, dmax) : NULL;
+    if (use_grid && !g) return -1;
+    double T[16], sums[ORC_NTERMS];
+    memcpy(T, T0, sizeof(T));
+    int32_t it = 0, fl = 0, conv = 0, passes = 0;
+
+    orc_pass(T, src, n, tgt, nrm, m, g, dmax, NULL, sums, NULL);
+    double cnt = sums[27];
+    double fit = cnt / (double)n, rmse = cnt > 0 ? sqrt(sums[28] / cnt) : 0.0;
+    if (hist_fit) hist_fit[passes] = fit;
+    if (hist_rmse) hist_rmse[passes] = rmse;
+    ++passes;
+    double fp = fit, rp = rmse;
+    while (it < max_iterations) {
+        if (cnt == 0.0) { fl |= ORC_FLAG_NO_CORR; break; }
+        double A[36], b[6], xi[6], dT[16];
+        orc_expand_jtj(sums, A);
+        for (int i = 0; i < 6; ++i) b[i] = -sums[21 + i];
+        if (cnt < 6.0 || orc_ldlt_solve(A, b, xi)) { fl |= ORC_FLAG_DEGENERATE; break; }
+        orc_exp_se3(xi, dT);
+        orc_compose(dT, T, T);
+        ++it;
+        orc_pass(T, src, n, tgt, nrm, m, g, dmax, NULL, sums, NULL);
+        cnt = sums[27];
+        fit = cnt / (double)n;
+        rmse = cnt > 0 ? sqrt(sums[28] / cnt) : 0.0;
+        if (hist_fit) hist_fit[passes] = fit;
+        if (hist_rmse) hist_rmse[passes] = rmse;
+        ++passes;
+        if (fabs(fit - fp) < relative_fitness && fabs(rmse - rp) < relative_rmse) { conv = 1; break; }
+        fp = fit;
+        rp = rmse;
+    }
+    if (cnt == 0.0) fl |= ORC_FLAG_NO_CORR;
+    memcpy(T_out, T, sizeof(T));
+    *fitness = fit;
+    *inlier_rmse = rmse;
+    *iterations = it;
+    *flags = fl;
+    *converged = conv;
+    orc_grid_free(g);
+    return passes;
+}

@@ -1,0 +1,186 @@
+/*
+ * o3g.h — C ABI of the B200-native point-to-plane ICP hot path.
+ *
+ * The operation is Open3D's registration_icp(source, target,
+ * max_correspondence_distance, init, TransformationEstimationPointToPlane())
+ * (§3.3): iterate { transform the source by T; find each
+ * source point's nearest target point within max_correspondence_distance;
+ * form the point-to-plane residual r = (T s - q).n and its 6-DoF Jacobian;
+ * reduce J^T J and J^T r; take the Gauss-Newton step of
+ * Eq. 2; compose } until the fitness / inlier-rmse criteria
+ * of SPEC.md:282-290 hold. Conventions are DESIGN.md §3's readings R1-R14.
+ *
+ * General rules (every entry point):
+ *  - Return an o3g_status; never throw, never abort. O3G_OK is 0.
+ *  - Point arrays are float32, row-major [n][3] (x,y,z), contiguous.
+ *    4x4 transforms are float64 row-major (16 doubles), rigid: R^T R = I and
+ *    det R = +1 within 1e-9, bottom row exactly (0,0,0,1).
+ *  - Array pointers may be DEVICE pointers (cudaMalloc / torch CUDA tensors,
+ *    on the context's device) or HOST pointers (pageable or pinned); the
+ *    library asks the driver which. Host arrays are copied to the device
+ *    inside the call (this is the "end-to-end" path). Scalars and 4x4
+ *    matrices are always host values.
+ *  - Ownership: the library never frees, retains or writes caller arrays
+ *    except the documented outputs. An o3g_ctx owns all device memory it
+ *    allocates; o3g_destroy releases it.
+ *  - Streams: work is ordered on the context's stream (cuda_stream; NULL =
+ *    the legacy default stream). Host outputs are valid on return: calls
+ *    that return host values synchronise that stream.
+ *  - Errors: O3G_ERR_INVALID_ARGUMENT for n <= 0 ("empty ->
+ *    invalid-argument"), dmax <= 0 or non-finite, NULL required pointers
+ *    (point-to-plane needs target normals), non-rigid T
+ *    (SPEC.md:80), negative criteria / iterations, non-finite coordinates
+ *    or normals ("non-finite"). O3G_ERR_CUDA / _OUT_OF_MEMORY /
+ *    _COMM report runtime failures; o3g_last_error() gives the message.
+ *  - Zero correspondences are not an error: O3G_OK, fitness
+ *    0, rmse 0, info.flags |= O3G_FLAG_NO_CORRESPONDENCES, T_out = last T.
+ *  - A singular 6x6 system stops the loop: O3G_OK with info.flags |=
+ *    O3G_FLAG_DEGENERATE and T_out = the last T (R6).
+ *  - There is no CPU fallback: without a usable sm_100a device every call
+ *    that needs one returns O3G_ERR_CUDA.
+ */
+#ifndef O3G_H
+#define O3G_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)
+#endif
+
+typedef enum {
+    O3G_OK = 0,
+    O3G_ERR_INVALID_ARGUMENT = 1,
+    O3G_ERR_DEGENERATE = 2,
+    O3G_ERR_CUDA = 3,
+    O3G_ERR_OUT_OF_MEMORY = 4,
+    O3G_ERR_COMM = 5,
+    O3G_ERR_NOT_IMPLEMENTED = 6
+} o3g_status;
+
+enum { O3G_FLAG_NO_CORRESPONDENCES = 1, O3G_FLAG_DEGENERATE = 2 };
+
+/* Number of reduction terms of one pass (R4):
+ * [0..20] J^T J upper triangle, row-major (i <= j); [21..26] J^T r;
+ * [27] inlier count; [28] sum of squared Euclidean distances d^2.       */
+#define O3G_NTERMS 29
+
+typedef struct {
+    int32_t iterations;  /* Gauss-Newton updates applied (<= max_iterations) */
+    int32_t passes;      /* correspondence passes run = iterations + 1 */
+    int32_t converged;   /* 1 if the S:285 criteria stopped the loop */
+    int32_t flags;       /* O3G_FLAG_* */
+    double fitness;      /* at T_out: inliers / n_source */
+    double inlier_rmse;  /* at T_out: sqrt(sum d^2 / inliers), 0 if none */
+    double inlier_count; /* at T_out */
+} o3g_icp_info;
+
+typedef struct o3g_ctx o3g_ctx;
+
+/* ---------------------------------------------------------------- one-shot
+ * registration_icp, point-to-plane.
+ * source_xyz [n_source][3], target_xyz / target_normals [n_target][3]:
+ * float32, host or device. Normals are used as given (R10).
+ * max_correspondence_distance: the inclusive radius dmax (R1).
+ * max_iterations: number of updates (>= 0). relative_fitness,
+ * relative_rmse: absolute-difference thresholds between consecutive passes
+ * with strict '<' (R8). Outputs (host): T_out[16], *fitness, *inlier_rmse,
+ * info (nullable). Uses a per-thread cached context on the current device.
+ */
+o3g_status o3g_icp_point_to_plane(const float* source_xyz, int64_t n_source,
+                                  const float* target_xyz, const float* target_normals,
+                                  int64_t n_target, const double init_T[16],
+                                  double max_correspondence_distance, int32_t max_iterations,
+                                  double relative_fitness, double relative_rmse, double T_out[16],
+                                  double* fitness, double* inlier_rmse, o3g_icp_info* info,
+                                  void* cuda_stream);
+
+/* --------------------------------------------------------------- stateful */
+/* Create a context on CUDA device `device`, ordered on `cuda_stream`.     */
+o3g_status o3g_create(o3g_ctx** out, int device, void* cuda_stream);
+o3g_status o3g_destroy(o3g_ctx* ctx);
+
+/* A1: build the voxel-hash grid over the target (cell size
+ * dmax*(1+2^-20)); keeps sorted float4 copies of xyz (+ original index)
+ * and normals. Invalidates any previously set source ordering.          */
+o3g_status o3g_set_target(o3g_ctx* ctx, const float* xyz, const float* normals, int64_t n,
+                          double max_correspondence_distance);
+
+/* A2: store the source, ordered by the grid cell of order_T * s (NULL =
+ * identity) for locality. Requires o3g_set_target first. The FULL source
+ * is passed on every rank; when distributed (o3g_dist_init) the context
+ * keeps its contiguous shard of the spatial order and the fitness
+ * denominator stays n (the global count).                               */
+o3g_status o3g_set_source(o3g_ctx* ctx, const float* xyz, int64_t n, const double order_T[16]);
+
+/* One correspondence + reduction pass at fixed T_in (north_star's
+ * o3g_icp_step). Outputs:
+ *   corr_out: DEVICE int32 [n] or NULL. Written in ORIGINAL source order
+ *     with ORIGINAL target indices; -1 = no target within dmax. When
+ *     distributed, only this rank's shard positions are written.
+ *   JTJ_out[36] (full symmetric, mirrored from 21 terms), JTr_out[6],
+ *   *inlier_count, *sum_sq_dist: host, nullable; summed over all ranks.
+ *   terms_out[O3G_NTERMS]: host, nullable, the raw 29 terms.             */
+o3g_status o3g_icp_step(o3g_ctx* ctx, const double T_in[16], int32_t* corr_out,
+                        double JTJ_out[36], double JTr_out[6], double* inlier_count,
+                        double* sum_sq_dist, double* terms_out);
+
+/* The full loop on device (CUDA graph of max_iterations+1 passes, T and the
+ * criteria state resident in device memory; one host sync at the end).
+ * hist_fitness / hist_rmse: host, nullable, capacity max_iterations+1,
+ * one entry per pass.                                                   */
+o3g_status o3g_icp_run(o3g_ctx* ctx, const double init_T[16], int32_t max_iterations,
+                       double relative_fitness, double relative_rmse, double T_out[16],
+                       double* fitness, double* inlier_rmse, o3g_icp_info* info,
+                       double* hist_fitness, double* hist_rmse);
+
+/* ------------------------------------------------------------ multi-GPU
+ * One process per GPU. Rank 0 calls o3g_nccl_unique_id (128 bytes), the
+ * caller broadcasts it (e.g. torch.distributed), every rank calls
+ * o3g_dist_init before o3g_set_source. Each pass then all-gathers the 29
+ * partial terms of every rank (232 B + padding per rank) and sums them in
+ * rank order on every rank, so T is bit-identical everywhere.
+ * NCCL is loaded at run time (libnccl.so.2); O3G_ERR_COMM if unavailable. */
+o3g_status o3g_nccl_unique_id(void* id_out_128);
+o3g_status o3g_dist_init(o3g_ctx* ctx, int rank, int world, const void* nccl_unique_id_128);
+
+/* -------------------------------------------------------------- options
+ * O3G_OPT_SEARCH: 0 = exact fp64 scan of every candidate, 1 = fp32
+ *   prefilter with a proven margin + exact fp64 decision (default). Both
+ *   give bit-identical correspondences.
+ * O3G_OPT_GRID: 0 = auto, 1 = force dense cell table, 2 = force hashed
+ *   cell table (collisions only add candidates; results are identical).
+ * O3G_OPT_TIMING: 1 = record CUDA events around every correspondence
+ *   kernel inside the run graph (read with o3g_last_run_kernel_ms).
+ * O3G_OPT_BLOCKS_PER_SM: override the persistent grid size (0 = auto).  */
+enum { O3G_OPT_SEARCH = 1, O3G_OPT_GRID = 2, O3G_OPT_TIMING = 3, O3G_OPT_BLOCKS_PER_SM = 4 };
+o3g_status o3g_set_option(o3g_ctx* ctx, int option, int64_t value);
+
+/* Sum of the correspondence-kernel (K3) durations of the last o3g_icp_run
+ * with O3G_OPT_TIMING=1, the number of K3 launches that did work, and the
+ * tail-kernel total. Milliseconds.                                      */
+o3g_status o3g_last_run_kernel_ms(o3g_ctx* ctx, double* k3_ms, int32_t* k3_launches,
+                                  double* tail_ms);
+
+/* Grid statistics of the current target: cells per axis, table entries,
+ * hashed (0/1), occupied cells. Any pointer may be NULL.                 */
+o3g_status o3g_grid_info(o3g_ctx* ctx, int64_t dims[3], int64_t* table_size, int32_t* hashed,
+                         int64_t* occupied_cells);
+
+/* Kernel launches issued by this context so far (all kinds).            */
+int64_t o3g_launch_count(const o3g_ctx* ctx);
+
+const char* o3g_status_string(o3g_status s);
+/* Last error message of the calling thread ("" if none).                */
+const char* o3g_last_error(void);
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+#ifdef __cplusplus
+}
+#endif
+#endif /* O3G_H */

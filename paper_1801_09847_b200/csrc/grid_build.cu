@@ -1,0 +1,161 @@
+// grid_build.cu — per-call kernels of the hot path:
+// target bounding box + finiteness check, cell keys, per-cell histogram
+// (cell start table via exclusive scan), and the gathers that lay the sorted
+// target / source out as float4 records for the correspondence kernel.
+#include <float.h>
+
+#include "o3g_internal.cuh"
+
+namespace o3g {
+
+// Order-preserving float <-> uint32 map, for atomicMin/atomicMax on floats.
+__device__ __forceinline__ uint32_t f2ord(float f) {
+    uint32_t b = __float_as_uint(f);
+    return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+
+__device__ __forceinline__ bool finite_f(float v) { return isfinite(v); }
+
+// A0/A1: componentwise min/max of the target and a non-finite flag.
+__global__ void k_bbox(const float* __restrict__ xyz, int64_t n, uint32_t* __restrict__ mm,
+                       int32_t* __restrict__ nonfinite) {
+    float lo[3] = {FLT_MAX, FLT_MAX, FLT_MAX}, hi[3] = {-FLT_MAX, -FLT_MAX, -FLT_MAX};
+    int bad = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            float v = xyz[3 * i + a];
+            bad |= !finite_f(v);
+            lo[a] = fminf(lo[a], v);
+            hi[a] = fmaxf(hi[a], v);
+        }
+    }
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        for (int o = 16; o; o >>= 1) {
+            lo[a] = fminf(lo[a], __shfl_xor_sync(0xffffffffu, lo[a], o));
+            hi[a] = fmaxf(hi[a], __shfl_xor_sync(0xffffffffu, hi[a], o));
+        }
+    }
+    bad = __any_sync(0xffffffffu, bad);
+    if ((threadIdx.x & 31) == 0) {
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            atomicMin(&mm[a], f2ord(lo[a]));
+            atomicMax(&mm[3 + a], f2ord(hi[a]));
+        }
+        if (bad) atomicOr(nonfinite, 1);
+    }
+}
+
+__global__ void k_check_finite(const float* __restrict__ v, int64_t count, int32_t* nonfinite) {
+    int bad = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+         i += (int64_t)gridDim.x * blockDim.x)
+        bad |= !finite_f(v[i]);
+    bad = __any_sync(0xffffffffu, bad);
+    if ((threadIdx.x & 31) == 0 && bad) atomicOr(nonfinite, 1);
+}
+
+// A1/A2: table index of the cell of each point (target: T = NULL, the raw
+// coordinates; source: the cell of T s, clamped into the grid — ordering
+// only, so clamping far points is harmless).
+__global__ void k_cell_keys(const float* __restrict__ xyz, int64_t n, GridDev g, bool has_T,
+                            double T0, double T1, double T2, double T3, double T4, double T5,
+                            double T6, double T7, double T8, double T9, double T10, double T11,
+                            uint32_t* __restrict__ keys, int32_t* __restrict__ vals) {
+    const double T[12] = {T0, T1, T2, T3, T4, T5, T6, T7, T8, T9, T10, T11};
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        float x = xyz[3 * i], y = xyz[3 * i + 1], z = xyz[3 * i + 2];
+        double sx = x, sy = y, sz = z;
+        if (has_T) xform_rn(T, x, y, z, sx, sy, sz);
+        int cx = min(max(cell_coord(sx, g.ox, g.inv_h, g.nx), 0), g.nx - 1);
+        int cy = min(max(cell_coord(sy, g.oy, g.inv_h, g.ny), 0), g.ny - 1);
+        int cz = min(max(cell_coord(sz, g.oz, g.inv_h, g.nz), 0), g.nz - 1);
+        uint32_t k = g.hashed ? ((grid_row_hash(cy, cz) + (uint32_t)cx) & g.hmask)
+                              : (uint32_t)grid_index_dense(g, cx, cy, cz);
+        keys[i] = k;
+        vals[i] = (int32_t)i;
+    }
+}
+
+__global__ void k_histogram(const uint32_t* __restrict__ keys, int64_t n, int32_t* counts) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        atomicAdd(&counts[keys[i]], 1);
+}
+
+__global__ void k_gather_target(const float* __restrict__ xyz, const float* __restrict__ nrm,
+                                const int32_t* __restrict__ vals, const uint32_t* __restrict__ keys,
+                                int64_t n, float4* __restrict__ tpos, float4* __restrict__ tnrm,
+                                unsigned long long* occupied) {
+    int occ = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int32_t v = vals[i];
+        tpos[i] = make_float4(xyz[3 * (int64_t)v], xyz[3 * (int64_t)v + 1], xyz[3 * (int64_t)v + 2],
+                              __int_as_float(v));
+        tnrm[i] = make_float4(nrm[3 * (int64_t)v], nrm[3 * (int64_t)v + 1], nrm[3 * (int64_t)v + 2], 0.f);
+        occ += (i == 0 || keys[i] != keys[i - 1]);
+    }
+    for (int o = 16; o; o >>= 1) occ += __shfl_xor_sync(0xffffffffu, occ, o);
+    if ((threadIdx.x & 31) == 0 && occ) atomicAdd(occupied, (unsigned long long)occ);
+}
+
+__global__ void k_gather_source(const float* __restrict__ xyz, const int32_t* __restrict__ vals,
+                                int64_t lo, int64_t hi, float4* __restrict__ out) {
+    for (int64_t i = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < hi;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int32_t v = vals[i];
+        out[i - lo] = make_float4(xyz[3 * (int64_t)v], xyz[3 * (int64_t)v + 1], xyz[3 * (int64_t)v + 2],
+                                  __int_as_float(v));
+    }
+}
+
+__global__ void k_fill_i32(int32_t* p, int64_t n, int32_t v) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        p[i] = v;
+}
+
+static int blocks_for(int64_t n, int threads, int cap = 148 * 16) {
+    int64_t b = (n + threads - 1) / threads;
+    if (b < 1) b = 1;
+    return (int)(b < cap ? b : cap);
+}
+
+void launch_bbox(const float* xyz, int64_t n, uint32_t* mm, int32_t* nonfinite, int sms,
+                 cudaStream_t s) {
+    k_bbox<<<blocks_for(n, 256, sms * 8), 256, 0, s>>>(xyz, n, mm, nonfinite);
+}
+void launch_check_finite(const float* v, int64_t count, int32_t* nonfinite, int sms,
+                         cudaStream_t s) {
+    k_check_finite<<<blocks_for(count, 256, sms * 8), 256, 0, s>>>(v, count, nonfinite);
+}
+void launch_cell_keys(const float* xyz, int64_t n, const GridDev& g, const double* T,
+                      uint32_t* keys, int32_t* vals, cudaStream_t s) {
+    static const double I[12] = {1, 0, 0, 0, 0, 1, 0, 0, 0, 0, 1, 0};
+    const double* t = T ? T : I;
+    k_cell_keys<<<blocks_for(n, 256), 256, 0, s>>>(xyz, n, g, T != nullptr, t[0], t[1], t[2], t[3],
+                                                   t[4], t[5], t[6], t[7], t[8], t[9], t[10], t[11],
+                                                   keys, vals);
+}
+void launch_histogram(const uint32_t* keys, int64_t n, int32_t* counts, cudaStream_t s) {
+    k_histogram<<<blocks_for(n, 256), 256, 0, s>>>(keys, n, counts);
+}
+void launch_gather_target(const float* xyz, const float* nrm, const int32_t* vals,
+                          const uint32_t* keys, int64_t n, float4* tpos, float4* tnrm,
+                          unsigned long long* occupied, cudaStream_t s) {
+    k_gather_target<<<blocks_for(n, 256), 256, 0, s>>>(xyz, nrm, vals, keys, n, tpos, tnrm, occupied);
+}
+void launch_gather_source(const float* xyz, const int32_t* vals, int64_t lo, int64_t hi,
+                          float4* out, cudaStream_t s) {
+    k_gather_source<<<blocks_for(hi - lo, 256), 256, 0, s>>>(xyz, vals, lo, hi, out);
+}
+void launch_fill_i32(int32_t* p, int64_t n, int32_t v, cudaStream_t s) {
+    k_fill_i32<<<blocks_for(n, 256), 256, 0, s>>>(p, n, v);
+}
+
+}  // namespace o3g

@@ -1,0 +1,747 @@
+// o3g_api.cu — the C ABI of include/o3g.h: argument validation, the
+// context (device buffers, grid build, source ordering), the graph-launched
+// iteration loop and the multi-GPU exchange (NCCL, loaded at run time).
+#include <dlfcn.h>
+#include <math.h>
+#include <string.h>
+
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+#include <string>
+#include <vector>
+
+#include "../../include/o3g.h"
+#include "o3g_internal.cuh"
+
+using namespace o3g;
+
+// --------------------------------------------------------------- errors
+static thread_local std::string g_err;
+
+static o3g_status fail(o3g_status s, const std::string& msg) {
+    g_err = msg;
+    return s;
+}
+
+#define CK(call)                                                                          \
+    do {                                                                                  \
+        cudaError_t e_ = (call);                                                          \
+        if (e_ != cudaSuccess) {                                                          \
+            cudaGetLastError();                                                           \
+            return fail(e_ == cudaErrorMemoryAllocation ? O3G_ERR_OUT_OF_MEMORY : O3G_ERR_CUDA, \
+                        std::string(#call) + ": " + cudaGetErrorString(e_));              \
+        }                                                                                 \
+    } while (0)
+
+#define TRY(expr)                          \
+    do {                                   \
+        o3g_status s_ = (expr);            \
+        if (s_ != O3G_OK) return s_;       \
+    } while (0)
+
+// --------------------------------------------------------- device buffers
+struct DevBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    o3g_status ensure(size_t bytes, bool* grew = nullptr) {
+        if (bytes <= cap && p) return O3G_OK;
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+        size_t b = bytes < 256 ? 256 : bytes;
+        cudaError_t e = cudaMalloc(&p, b);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            return fail(O3G_ERR_OUT_OF_MEMORY, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+        }
+        cap = b;
+        if (grew) *grew = true;
+        return O3G_OK;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
+    template <class T>
+    T* as() const { return (T*)p; }
+};
+
+// ------------------------------------------------------------------ NCCL
+namespace {
+typedef int nccl_result_t;
+typedef void* nccl_comm_t;
+struct nccl_uid { char internal[128]; };
+struct NcclApi {
+    bool loaded = false;
+    nccl_result_t (*get_unique_id)(nccl_uid*) = nullptr;
+    nccl_result_t (*comm_init_rank)(nccl_comm_t*, int, nccl_uid, int) = nullptr;
+    nccl_result_t (*all_gather)(const void*, void*, size_t, int, nccl_comm_t, cudaStream_t) = nullptr;
+    nccl_result_t (*comm_destroy)(nccl_comm_t) = nullptr;
+    const char* (*error_string)(nccl_result_t) = nullptr;
+};
+constexpr int kNcclFloat64 = 8;
+
+NcclApi& nccl() {
+    static NcclApi api;
+    if (!api.loaded) {
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (h) {
+            api.get_unique_id = (decltype(api.get_unique_id))dlsym(h, "ncclGetUniqueId");
+            api.comm_init_rank = (decltype(api.comm_init_rank))dlsym(h, "ncclCommInitRank");
+            api.all_gather = (decltype(api.all_gather))dlsym(h, "ncclAllGather");
+            api.comm_destroy = (decltype(api.comm_destroy))dlsym(h, "ncclCommDestroy");
+            api.error_string = (decltype(api.error_string))dlsym(h, "ncclGetErrorString");
+            api.loaded = api.get_unique_id && api.comm_init_rank && api.all_gather && api.comm_destroy;
+        }
+    }
+    return api;
+}
+}  // namespace
+
+// ------------------------------------------------------------------ ctx
+struct GraphKey {
+    int max_it = -1, search = -1, timing = -1, world = -1, blocks = -1;
+    int64_t n_local = -1;
+    const void* ptrs[8] = {};
+    bool operator==(const GraphKey& o) const {
+        return max_it == o.max_it && search == o.search && timing == o.timing && world == o.world &&
+               blocks == o.blocks && n_local == o.n_local && !memcmp(ptrs, o.ptrs, sizeof(ptrs));
+    }
+};
+
+struct o3g_ctx {
+    int device = 0;
+    int sms = 148;
+    cudaStream_t user = nullptr;   // caller's stream (may be the legacy default)
+    cudaStream_t exec = nullptr;   // internal capture/execution stream
+    cudaEvent_t fence = nullptr;
+
+    // options
+    int search = 1, grid_mode = 0, timing = 0, bps_override = 0;
+
+    // target grid
+    int64_t m = 0;
+    double dmax = 0.0;
+    GridDev g{};
+    int64_t occupied = 0;
+    DevBuf tpos, tnrm, cell_start, counts;
+    // scratch
+    DevBuf keys_a, keys_b, vals_a, vals_b, cub_tmp, stage_a, stage_b, misc;
+    // source
+    int64_t n_total = 0, n_local = 0, shard_lo = 0;
+    bool src_ready = false;
+    DevBuf src4;
+    // loop
+    DevBuf partials, gathered, state, hist_fit, hist_rmse;
+    IcpState* h_state = nullptr;   // pinned
+    // graph
+    cudaGraphExec_t gexec = nullptr;
+    GraphKey gkey;
+    std::vector<cudaEvent_t> events;
+    int graph_launches = 0;        // our kernels per graph launch
+    // distributed
+    int rank = 0, world = 1;
+    nccl_comm_t comm = nullptr;
+    // stats
+    int64_t launches = 0;
+    double last_k3_ms = 0.0, last_tail_ms = 0.0;
+    int32_t last_k3_launches = 0;
+};
+
+// ------------------------------------------------------------- helpers
+static bool is_device_ptr(const void* p) {
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+static bool rigid_ok(const double* T) {
+    if (!T) return false;
+    for (int i = 0; i < 16; ++i)
+        if (!isfinite(T[i])) return false;
+    if (T[12] != 0.0 || T[13] != 0.0 || T[14] != 0.0 || T[15] != 1.0) return false;
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) {
+            double s = 0.0;
+            for (int k = 0; k < 3; ++k) s += T[4 * k + i] * T[4 * k + j];
+            if (fabs(s - (i == j ? 1.0 : 0.0)) > 1e-9) return false;
+        }
+    const double det = T[0] * (T[5] * T[10] - T[6] * T[9]) - T[1] * (T[4] * T[10] - T[6] * T[8]) +
+                       T[2] * (T[4] * T[9] - T[5] * T[8]);
+    return fabs(det - 1.0) <= 1e-9;
+}
+
+static float ord2f(uint32_t u) {
+    uint32_t b = (u & 0x80000000u) ? (u & 0x7fffffffu) : ~u;
+    float f;
+    memcpy(&f, &b, 4);
+    return f;
+}
+
+// Fence: work on ctx->exec starts after everything already on the user stream.
+static o3g_status enter(o3g_ctx* c) {
+    CK(cudaSetDevice(c->device));
+    CK(cudaEventRecord(c->fence, c->user));
+    CK(cudaStreamWaitEvent(c->exec, c->fence, 0));
+    return O3G_OK;
+}
+
+// Device view of an input array: the caller's pointer if it is device
+// memory, else a copy into a context staging buffer (the e2e path).
+static o3g_status device_view(o3g_ctx* c, const float* p, int64_t count, DevBuf& stage,
+                              const float** out) {
+    if (is_device_ptr(p)) {
+        *out = p;
+        return O3G_OK;
+    }
+    TRY(stage.ensure((size_t)count * sizeof(float)));
+    CK(cudaMemcpyAsync(stage.p, p, (size_t)count * sizeof(float), cudaMemcpyHostToDevice, c->exec));
+    *out = stage.as<float>();
+    return O3G_OK;
+}
+
+static int bits_for(uint64_t maxval) {
+    int b = 1;
+    while (b < 32 && (maxval >> b)) ++b;
+    return b;
+}
+
+static o3g_status sort_pairs(o3g_ctx* c, int64_t n, int end_bit) {
+    size_t tmp = 0;
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp, c->keys_a.as<uint32_t>(), c->keys_b.as<uint32_t>(),
+                                       c->vals_a.as<int32_t>(), c->vals_b.as<int32_t>(), (int)n, 0,
+                                       end_bit, c->exec));
+    TRY(c->cub_tmp.ensure(tmp));
+    CK(cub::DeviceRadixSort::SortPairs(c->cub_tmp.p, tmp, c->keys_a.as<uint32_t>(), c->keys_b.as<uint32_t>(),
+                                       c->vals_a.as<int32_t>(), c->vals_b.as<int32_t>(), (int)n, 0,
+                                       end_bit, c->exec));
+    return O3G_OK;
+}
+
+static void invalidate_graph(o3g_ctx* c) {
+    if (c->gexec) cudaGraphExecDestroy(c->gexec);
+    c->gexec = nullptr;
+    c->gkey = GraphKey{};
+}
+
+// ------------------------------------------------------------- C ABI
+extern "C" {
+
+const char* o3g_status_string(o3g_status s) {
+    switch (s) {
+        case O3G_OK: return "ok";
+        case O3G_ERR_INVALID_ARGUMENT: return "invalid argument";
+        case O3G_ERR_DEGENERATE: return "degenerate input";
+        case O3G_ERR_CUDA: return "cuda error";
+        case O3G_ERR_OUT_OF_MEMORY: return "out of memory";
+        case O3G_ERR_COMM: return "communication error";
+        case O3G_ERR_NOT_IMPLEMENTED: return "not implemented";
+    }
+    return "unknown status";
+}
+
+const char* o3g_last_error(void) { return g_err.c_str(); }
+
+o3g_status o3g_create(o3g_ctx** out, int device, void* cuda_stream) {
+    if (!out) return fail(O3G_ERR_INVALID_ARGUMENT, "out is NULL");
+    *out = nullptr;
+    int ndev = 0;
+    CK(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) return fail(O3G_ERR_INVALID_ARGUMENT, "bad device index");
+    CK(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10) return fail(O3G_ERR_CUDA, "o3g is built for sm_100a (B200) only");
+    o3g_ctx* c = new o3g_ctx();
+    c->device = device;
+    c->sms = prop.multiProcessorCount;
+    c->user = (cudaStream_t)cuda_stream;
+    cudaError_t e = cudaStreamCreate(&c->exec);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->fence, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaMallocHost(&c->h_state, sizeof(IcpState));
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        o3g_destroy(c);
+        return fail(O3G_ERR_CUDA, std::string("context setup: ") + cudaGetErrorString(e));
+    }
+    *out = c;
+    return O3G_OK;
+}
+
+o3g_status o3g_destroy(o3g_ctx* c) {
+    if (!c) return O3G_OK;
+    cudaSetDevice(c->device);
+    if (c->exec) cudaStreamSynchronize(c->exec);
+    invalidate_graph(c);
+    for (auto ev : c->events) cudaEventDestroy(ev);
+    DevBuf* bufs[] = {&c->tpos, &c->tnrm, &c->cell_start, &c->counts, &c->keys_a, &c->keys_b,
+                      &c->vals_a, &c->vals_b, &c->cub_tmp, &c->stage_a, &c->stage_b, &c->misc,
+                      &c->src4, &c->partials, &c->gathered, &c->state, &c->hist_fit, &c->hist_rmse};
+    for (DevBuf* b : bufs) b->release();
+    if (c->comm && nccl().comm_destroy) nccl().comm_destroy(c->comm);
+    if (c->h_state) cudaFreeHost(c->h_state);
+    if (c->fence) cudaEventDestroy(c->fence);
+    if (c->exec) cudaStreamDestroy(c->exec);
+    delete c;
+    return O3G_OK;
+}
+
+o3g_status o3g_set_option(o3g_ctx* c, int option, int64_t value) {
+    if (!c) return fail(O3G_ERR_INVALID_ARGUMENT, "ctx is NULL");
+    switch (option) {
+        case O3G_OPT_SEARCH:
+            if (value < 0 || value > 1) return fail(O3G_ERR_INVALID_ARGUMENT, "search must be 0 or 1");
+            c->search = (int)value;
+            break;
+        case O3G_OPT_GRID:
+            if (value < 0 || value > 2) return fail(O3G_ERR_INVALID_ARGUMENT, "grid must be 0, 1 or 2");
+            c->grid_mode = (int)value;
+            break;
+        case O3G_OPT_TIMING: c->timing = value ? 1 : 0; break;
+        case O3G_OPT_BLOCKS_PER_SM:
+            if (value < 0 || value > 64) return fail(O3G_ERR_INVALID_ARGUMENT, "blocks per SM out of range");
+            c->bps_override = (int)value;
+            break;
+        default: return fail(O3G_ERR_INVALID_ARGUMENT, "unknown option");
+    }
+    invalidate_graph(c);
+    return O3G_OK;
+}
+
+o3g_status o3g_set_target(o3g_ctx* c, const float* xyz, const float* normals, int64_t n,
+                          double dmax) {
+    if (!c) return fail(O3G_ERR_INVALID_ARGUMENT, "ctx is NULL");
+    if (!xyz || !normals) return fail(O3G_ERR_INVALID_ARGUMENT, "target xyz and normals are required");
+    if (n <= 0 || n > 0x7ffffffeLL) return fail(O3G_ERR_INVALID_ARGUMENT, "n_target must be in [1, 2^31-2]");
+    if (!(dmax > 0.0) || !isfinite(dmax)) return fail(O3G_ERR_INVALID_ARGUMENT, "max_correspondence_distance must be finite and > 0");
+    TRY(enter(c));
+    c->src_ready = false;
+    c->m = 0;
+    invalidate_graph(c);
+    const float *dx, *dn;
+    TRY(device_view(c, xyz, 3 * n, c->stage_a, &dx));
+    TRY(device_view(c, normals, 3 * n, c->stage_b, &dn));
+
+    // A0/A1: bbox + finiteness (one sync: the grid dims size the table)
+    TRY(c->misc.ensure(64));
+    uint32_t* mm = c->misc.as<uint32_t>();
+    int32_t* bad = (int32_t*)(mm + 6);
+    unsigned long long* occ = (unsigned long long*)(mm + 8);
+    CK(cudaMemsetAsync(mm, 0xFF, 12, c->exec));
+    CK(cudaMemsetAsync(mm + 3, 0x00, 12 + 4 + 4 + 8, c->exec));
+    launch_bbox(dx, n, mm, bad, c->sms, c->exec);
+    launch_check_finite(dn, 3 * n, bad, c->sms, c->exec);
+    c->launches += 2;
+    uint32_t h[8];
+    CK(cudaMemcpyAsync(h, mm, 32, cudaMemcpyDeviceToHost, c->exec));
+    CK(cudaStreamSynchronize(c->exec));
+    if (h[6]) return fail(O3G_ERR_INVALID_ARGUMENT, "non-finite target coordinate or normal");
+
+    GridDev g{};
+    const double hcell = dmax * (1.0 + 9.5367431640625e-07);  // dmax (1 + 2^-20), R12
+    g.inv_h = 1.0 / hcell;
+    double o[3];
+    int64_t dims[3];
+    for (int a = 0; a < 3; ++a) {
+        o[a] = (double)ord2f(h[a]);
+        double hi = (double)ord2f(h[3 + a]);
+        double cmax = floor((hi - o[a]) * g.inv_h);
+        if (!(cmax < 1073741824.0)) return fail(O3G_ERR_INVALID_ARGUMENT, "target extent / dmax exceeds 2^30 cells per axis");
+        dims[a] = (int64_t)cmax + 1;
+    }
+    g.ox = o[0], g.oy = o[1], g.oz = o[2];
+    g.nx = (int32_t)dims[0], g.ny = (int32_t)dims[1], g.nz = (int32_t)dims[2];
+    const double ncells = (double)dims[0] * (double)dims[1] * (double)dims[2];
+    const double dense_cap = fmax(64.0 * (double)n, 16777216.0);
+    bool hashed = c->grid_mode == 2 || (c->grid_mode == 0 && ncells > dense_cap) || ncells > 2147483000.0;
+    if (hashed) {
+        uint64_t t = 1024;
+        while (t < 2ull * (uint64_t)n) t <<= 1;
+        g.hashed = 1;
+        g.hmask = (uint32_t)(t - 1);
+        g.table_size = (int64_t)t;
+    } else {
+        g.hashed = 0;
+        g.hmask = 0;
+        g.table_size = (int64_t)ncells;
+    }
+
+    TRY(c->keys_a.ensure(n * 4));
+    TRY(c->keys_b.ensure(n * 4));
+    TRY(c->vals_a.ensure(n * 4));
+    TRY(c->vals_b.ensure(n * 4));
+    TRY(c->cell_start.ensure((g.table_size + 1) * 4));
+    TRY(c->counts.ensure((g.table_size + 1) * 4));
+    TRY(c->tpos.ensure(n * sizeof(float4)));
+    TRY(c->tnrm.ensure(n * sizeof(float4)));
+
+    launch_cell_keys(dx, n, g, nullptr, c->keys_a.as<uint32_t>(), c->vals_a.as<int32_t>(), c->exec);
+    TRY(sort_pairs(c, n, bits_for((uint64_t)(g.table_size - 1))));
+    CK(cudaMemsetAsync(c->counts.p, 0, (g.table_size + 1) * 4, c->exec));
+    launch_histogram(c->keys_a.as<uint32_t>(), n, c->counts.as<int32_t>(), c->exec);
+    size_t tmp = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, c->counts.as<int32_t>(), c->cell_start.as<int32_t>(),
+                                     (int)(g.table_size + 1), c->exec));
+    TRY(c->cub_tmp.ensure(tmp));
+    CK(cub::DeviceScan::ExclusiveSum(c->cub_tmp.p, tmp, c->counts.as<int32_t>(), c->cell_start.as<int32_t>(),
+                                     (int)(g.table_size + 1), c->exec));
+    launch_gather_target(dx, dn, c->vals_b.as<int32_t>(), c->keys_b.as<uint32_t>(), n,
+                         c->tpos.as<float4>(), c->tnrm.as<float4>(), occ, c->exec);
+    c->launches += 3;
+    unsigned long long h_occ = 0;
+    CK(cudaMemcpyAsync(&h_occ, occ, 8, cudaMemcpyDeviceToHost, c->exec));
+    CK(cudaStreamSynchronize(c->exec));
+    CK(cudaGetLastError());
+    c->g = g;
+    c->m = n;
+    c->dmax = dmax;
+    c->occupied = (int64_t)h_occ;
+    return O3G_OK;
+}
+
+o3g_status o3g_set_source(o3g_ctx* c, const float* xyz, int64_t n, const double order_T[16]) {
+    if (!c) return fail(O3G_ERR_INVALID_ARGUMENT, "ctx is NULL");
+    if (!xyz) return fail(O3G_ERR_INVALID_ARGUMENT, "source xyz is required");
+    if (n <= 0 || n > 0x7ffffffeLL) return fail(O3G_ERR_INVALID_ARGUMENT, "n_source must be in [1, 2^31-2]");
+    if (c->m <= 0) return fail(O3G_ERR_INVALID_ARGUMENT, "o3g_set_target must be called first");
+    if (order_T && !rigid_ok(order_T)) return fail(O3G_ERR_INVALID_ARGUMENT, "order_T is not a rigid transform");
+    TRY(enter(c));
+    c->src_ready = false;
+    invalidate_graph(c);
+    const float* dx;
+    TRY(device_view(c, xyz, 3 * n, c->stage_a, &dx));
+    TRY(c->misc.ensure(64));
+    int32_t* bad = (int32_t*)(c->misc.as<uint32_t>() + 6);
+    CK(cudaMemsetAsync(bad, 0, 4, c->exec));
+    launch_check_finite(dx, 3 * n, bad, c->sms, c->exec);
+    int32_t h_bad = 0;
+    CK(cudaMemcpyAsync(&h_bad, bad, 4, cudaMemcpyDeviceToHost, c->exec));
+    CK(cudaStreamSynchronize(c->exec));
+    if (h_bad) return fail(O3G_ERR_INVALID_ARGUMENT, "non-finite source coordinate");
+
+    TRY(c->keys_a.ensure(n * 4));
+    TRY(c->keys_b.ensure(n * 4));
+    TRY(c->vals_a.ensure(n * 4));
+    TRY(c->vals_b.ensure(n * 4));
+    double T12[12];
+    if (order_T) memcpy(T12, order_T, sizeof(T12));
+    launch_cell_keys(dx, n, c->g, order_T ? T12 : nullptr, c->keys_a.as<uint32_t>(),
+                     c->vals_a.as<int32_t>(), c->exec);
+    TRY(sort_pairs(c, n, bits_for((uint64_t)(c->g.table_size - 1))));
+    const int64_t lo = (int64_t)c->rank * n / c->world, hi = (int64_t)(c->rank + 1) * n / c->world;
+    TRY(c->src4.ensure((size_t)(hi - lo > 0 ? hi - lo : 1) * sizeof(float4)));
+    if (hi > lo) launch_gather_source(dx, c->vals_b.as<int32_t>(), lo, hi, c->src4.as<float4>(), c->exec);
+    c->launches += 3;
+    CK(cudaStreamSynchronize(c->exec));
+    CK(cudaGetLastError());
+    c->n_total = n;
+    c->n_local = hi - lo;
+    c->shard_lo = lo;
+    c->src_ready = true;
+    return O3G_OK;
+}
+
+static int k3_blocks(o3g_ctx* c, bool prefilter, bool write_corr) {
+    int bps = c->bps_override ? c->bps_override : k3_max_blocks_per_sm(prefilter, write_corr);
+    if (bps < 1) bps = 1;
+    int64_t need = (c->n_local + kK3Threads - 1) / kK3Threads;
+    int64_t b = (int64_t)c->sms * bps;
+    if (need < b) b = need;
+    return (int)(b < 1 ? 1 : b);
+}
+
+static o3g_status loop_buffers(o3g_ctx* c, int blocks, int hist_cap) {
+    TRY(c->partials.ensure((size_t)blocks * kTermStride * sizeof(double)));
+    TRY(c->gathered.ensure((size_t)c->world * kTermStride * sizeof(double)));
+    TRY(c->state.ensure(sizeof(IcpState)));
+    TRY(c->hist_fit.ensure((size_t)(hist_cap > 0 ? hist_cap : 1) * sizeof(double)));
+    TRY(c->hist_rmse.ensure((size_t)(hist_cap > 0 ? hist_cap : 1) * sizeof(double)));
+    return O3G_OK;
+}
+
+static K3Args k3_args(o3g_ctx* c, int32_t* corr) {
+    K3Args a;
+    a.src = c->src4.as<float4>();
+    a.n = (int32_t)c->n_local;
+    a.tpos = c->tpos.as<float4>();
+    a.tnrm = c->tnrm.as<float4>();
+    a.cell_start = c->cell_start.as<int32_t>();
+    a.g = c->g;
+    a.r2 = c->dmax * c->dmax;
+    a.dmax = c->dmax;
+    a.inv_dmax = 1.0 / c->dmax;
+    a.st = c->state.as<IcpState>();
+    a.block_partials = c->partials.as<double>();
+    a.corr_out = corr;
+    return a;
+}
+
+// One pass: K3, then the tail (with the rank exchange when distributed).
+static o3g_status enqueue_pass(o3g_ctx* c, int blocks, bool write_corr, int32_t* corr,
+                               int tail_mode, cudaEvent_t ev0, cudaEvent_t ev1, int* nlaunch) {
+    const bool prefilter = c->search == 1;
+    if (ev0) CK(cudaEventRecordWithFlags(ev0, c->exec, cudaEventRecordExternal));
+    if (c->n_local > 0) {
+        launch_k3(k3_args(c, corr), blocks, prefilter, write_corr, c->exec);
+        ++*nlaunch;
+    }
+    if (ev1) CK(cudaEventRecordWithFlags(ev1, c->exec, cudaEventRecordExternal));
+    const int nb = c->n_local > 0 ? blocks : 0;
+    double* gat = c->gathered.as<double>();
+    IcpState* st = c->state.as<IcpState>();
+    if (c->world == 1) {
+        launch_tail(c->partials.as<double>(), nb, gat, 1, 0, st, c->hist_fit.as<double>(),
+                    c->hist_rmse.as<double>(), TAIL_REDUCE_BLOCKS | tail_mode, c->exec);
+        ++*nlaunch;
+    } else {
+        launch_tail(c->partials.as<double>(), nb, gat, c->world, c->rank, st, nullptr, nullptr,
+                    TAIL_REDUCE_BLOCKS | TAIL_WRITE_RANK | (tail_mode & TAIL_STEP), c->exec);
+        nccl_result_t r = nccl().all_gather(gat + (size_t)c->rank * kTermStride, gat, kTermStride,
+                                            kNcclFloat64, c->comm, c->exec);
+        if (r != 0) return fail(O3G_ERR_COMM, std::string("ncclAllGather: ") +
+                                                  (nccl().error_string ? nccl().error_string(r) : "?"));
+        launch_tail(nullptr, 0, gat, c->world, c->rank, st, c->hist_fit.as<double>(),
+                    c->hist_rmse.as<double>(), TAIL_SUM_RANKS | tail_mode, c->exec);
+        *nlaunch += 2;
+    }
+    return O3G_OK;
+}
+
+static void init_state(o3g_ctx* c, const double* T, int max_it, double ef, double er, int cap) {
+    IcpState* s = c->h_state;
+    memset(s, 0, sizeof(IcpState));
+    memcpy(s->T, T, 16 * sizeof(double));
+    s->max_it = max_it;
+    s->rel_fit = ef;
+    s->rel_rmse = er;
+    s->n_total = (double)c->n_total;
+    s->hist_cap = cap;
+}
+
+o3g_status o3g_icp_step(o3g_ctx* c, const double T_in[16], int32_t* corr_out, double JTJ_out[36],
+                        double JTr_out[6], double* inlier_count, double* sum_sq_dist,
+                        double* terms_out) {
+    if (!c) return fail(O3G_ERR_INVALID_ARGUMENT, "ctx is NULL");
+    if (!rigid_ok(T_in)) return fail(O3G_ERR_INVALID_ARGUMENT, "T_in is not a rigid transform");
+    if (!c->src_ready) return fail(O3G_ERR_INVALID_ARGUMENT, "o3g_set_target and o3g_set_source must be called first");
+    if (corr_out && !is_device_ptr(corr_out)) return fail(O3G_ERR_INVALID_ARGUMENT, "corr_out must be device memory");
+    TRY(enter(c));
+    const bool wc = corr_out != nullptr;
+    const int blocks = k3_blocks(c, c->search == 1, wc);
+    TRY(loop_buffers(c, blocks, 1));
+    init_state(c, T_in, 0, 0.0, 0.0, 1);
+    CK(cudaMemcpyAsync(c->state.p, c->h_state, sizeof(IcpState), cudaMemcpyHostToDevice, c->exec));
+    int nl = 0;
+    TRY(enqueue_pass(c, blocks, wc, corr_out, TAIL_STEP, nullptr, nullptr, &nl));
+    c->launches += nl;
+    CK(cudaMemcpyAsync(c->h_state, c->state.p, sizeof(IcpState), cudaMemcpyDeviceToHost, c->exec));
+    CK(cudaStreamSynchronize(c->exec));
+    CK(cudaGetLastError());
+    const double* t = c->h_state->terms;
+    if (JTJ_out) {
+        int k = 0;
+        for (int i = 0; i < 6; ++i)
+            for (int j = i; j < 6; ++j) {
+                JTJ_out[6 * i + j] = t[k];
+                JTJ_out[6 * j + i] = t[k];
+                ++k;
+            }
+    }
+    if (JTr_out) memcpy(JTr_out, t + 21, 6 * sizeof(double));
+    if (inlier_count) *inlier_count = t[27];
+    if (sum_sq_dist) *sum_sq_dist = t[28];
+    if (terms_out) memcpy(terms_out, t, kTerms * sizeof(double));
+    return O3G_OK;
+}
+
+static o3g_status build_graph(o3g_ctx* c, int max_it, int blocks) {
+    GraphKey key;
+    key.max_it = max_it;
+    key.search = c->search;
+    key.timing = c->timing;
+    key.world = c->world;
+    key.blocks = blocks;
+    key.n_local = c->n_local;
+    const void* ptrs[8] = {c->src4.p, c->tpos.p, c->tnrm.p, c->cell_start.p, c->partials.p,
+                           c->state.p, c->hist_fit.p, c->gathered.p};
+    memcpy(key.ptrs, ptrs, sizeof(ptrs));
+    if (c->gexec && c->gkey == key) return O3G_OK;
+    invalidate_graph(c);
+    const size_t nev = c->timing ? 2 * (size_t)(max_it + 1) : 0;
+    while (c->events.size() < nev) {
+        cudaEvent_t ev;
+        CK(cudaEventCreate(&ev));
+        c->events.push_back(ev);
+    }
+    CK(cudaStreamBeginCapture(c->exec, cudaStreamCaptureModeThreadLocal));
+    int nl = 0;
+    o3g_status st = O3G_OK;
+    for (int p = 0; p <= max_it && st == O3G_OK; ++p)
+        st = enqueue_pass(c, blocks, false, nullptr, TAIL_SOLVE,
+                          c->timing ? c->events[2 * p] : nullptr,
+                          c->timing ? c->events[2 * p + 1] : nullptr, &nl);
+    cudaGraph_t graph = nullptr;
+    cudaError_t e = cudaStreamEndCapture(c->exec, &graph);
+    if (st != O3G_OK) {
+        if (graph) cudaGraphDestroy(graph);
+        return st;
+    }
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(O3G_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(e));
+    }
+    e = cudaGraphInstantiate(&c->gexec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        c->gexec = nullptr;
+        return fail(O3G_ERR_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
+    }
+    c->gkey = key;
+    c->graph_launches = nl;
+    return O3G_OK;
+}
+
+o3g_status o3g_icp_run(o3g_ctx* c, const double init_T[16], int32_t max_iterations,
+                       double relative_fitness, double relative_rmse, double T_out[16],
+                       double* fitness, double* inlier_rmse, o3g_icp_info* info,
+                       double* hist_fitness, double* hist_rmse) {
+    if (!c) return fail(O3G_ERR_INVALID_ARGUMENT, "ctx is NULL");
+    if (!rigid_ok(init_T)) return fail(O3G_ERR_INVALID_ARGUMENT, "init_T is not a rigid transform");
+    if (max_iterations < 0 || max_iterations > 100000) return fail(O3G_ERR_INVALID_ARGUMENT, "max_iterations must be in [0, 100000]");
+    if (!(relative_fitness >= 0.0) || !(relative_rmse >= 0.0)) return fail(O3G_ERR_INVALID_ARGUMENT, "criteria must be >= 0");
+    if (!c->src_ready) return fail(O3G_ERR_INVALID_ARGUMENT, "o3g_set_target and o3g_set_source must be called first");
+    if (!T_out || !fitness || !inlier_rmse) return fail(O3G_ERR_INVALID_ARGUMENT, "T_out, fitness and inlier_rmse are required");
+    TRY(enter(c));
+    const int blocks = k3_blocks(c, c->search == 1, false);
+    TRY(loop_buffers(c, blocks, max_iterations + 1));
+    init_state(c, init_T, max_iterations, relative_fitness, relative_rmse, max_iterations + 1);
+    CK(cudaMemcpyAsync(c->state.p, c->h_state, sizeof(IcpState), cudaMemcpyHostToDevice, c->exec));
+    TRY(build_graph(c, max_iterations, blocks));
+    CK(cudaGraphLaunch(c->gexec, c->exec));
+    c->launches += c->graph_launches;
+    CK(cudaMemcpyAsync(c->h_state, c->state.p, sizeof(IcpState), cudaMemcpyDeviceToHost, c->exec));
+    CK(cudaStreamSynchronize(c->exec));
+    CK(cudaGetLastError());
+    const IcpState* s = c->h_state;
+    const int passes = s->passes;
+    if (hist_fitness && passes > 0)
+        CK(cudaMemcpy(hist_fitness, c->hist_fit.p, passes * sizeof(double), cudaMemcpyDeviceToHost));
+    if (hist_rmse && passes > 0)
+        CK(cudaMemcpy(hist_rmse, c->hist_rmse.p, passes * sizeof(double), cudaMemcpyDeviceToHost));
+    memcpy(T_out, s->T, 16 * sizeof(double));
+    *fitness = s->fit;
+    *inlier_rmse = s->rmse;
+    if (info) {
+        info->iterations = s->it;
+        info->passes = passes;
+        info->converged = s->converged;
+        info->flags = s->flags;
+        info->fitness = s->fit;
+        info->inlier_rmse = s->rmse;
+        info->inlier_count = s->terms[27];
+    }
+    c->last_k3_ms = 0.0;
+    c->last_tail_ms = 0.0;
+    c->last_k3_launches = 0;
+    if (c->timing) {
+        for (int p = 0; p < passes; ++p) {
+            float ms = 0.f;
+            CK(cudaEventElapsedTime(&ms, c->events[2 * p], c->events[2 * p + 1]));
+            c->last_k3_ms += ms;
+            if (p + 1 < passes) {
+                CK(cudaEventElapsedTime(&ms, c->events[2 * p + 1], c->events[2 * p + 2]));
+                c->last_tail_ms += ms;
+            }
+        }
+        c->last_k3_launches = passes;
+    }
+    return O3G_OK;
+}
+
+o3g_status o3g_last_run_kernel_ms(o3g_ctx* c, double* k3_ms, int32_t* k3_launches, double* tail_ms) {
+    if (!c) return fail(O3G_ERR_INVALID_ARGUMENT, "ctx is NULL");
+    if (k3_ms) *k3_ms = c->last_k3_ms;
+    if (k3_launches) *k3_launches = c->last_k3_launches;
+    if (tail_ms) *tail_ms = c->last_tail_ms;
+    return O3G_OK;
+}
+
+o3g_status o3g_grid_info(o3g_ctx* c, int64_t dims[3], int64_t* table_size, int32_t* hashed,
+                         int64_t* occupied_cells) {
+    if (!c) return fail(O3G_ERR_INVALID_ARGUMENT, "ctx is NULL");
+    if (c->m <= 0) return fail(O3G_ERR_INVALID_ARGUMENT, "no target set");
+    if (dims) dims[0] = c->g.nx, dims[1] = c->g.ny, dims[2] = c->g.nz;
+    if (table_size) *table_size = c->g.table_size;
+    if (hashed) *hashed = c->g.hashed;
+    if (occupied_cells) *occupied_cells = c->occupied;
+    return O3G_OK;
+}
+
+int64_t o3g_launch_count(const o3g_ctx* c) { return c ? c->launches : 0; }
+
+o3g_status o3g_nccl_unique_id(void* id_out) {
+    if (!id_out) return fail(O3G_ERR_INVALID_ARGUMENT, "id_out is NULL");
+    if (!nccl().loaded) return fail(O3G_ERR_COMM, "libnccl.so.2 not loadable");
+    nccl_uid id;
+    nccl_result_t r = nccl().get_unique_id(&id);
+    if (r != 0) return fail(O3G_ERR_COMM, "ncclGetUniqueId failed");
+    memcpy(id_out, &id, sizeof(id));
+    return O3G_OK;
+}
+
+o3g_status o3g_dist_init(o3g_ctx* c, int rank, int world, const void* id) {
+    if (!c) return fail(O3G_ERR_INVALID_ARGUMENT, "ctx is NULL");
+    if (world < 1 || rank < 0 || rank >= world) return fail(O3G_ERR_INVALID_ARGUMENT, "bad rank/world");
+    if (world > 1 && !id) return fail(O3G_ERR_INVALID_ARGUMENT, "nccl unique id required");
+    CK(cudaSetDevice(c->device));
+    invalidate_graph(c);
+    c->src_ready = false;
+    if (c->comm && nccl().comm_destroy) nccl().comm_destroy(c->comm);
+    c->comm = nullptr;
+    c->rank = rank;
+    c->world = world;
+    if (world == 1) return O3G_OK;
+    if (!nccl().loaded) return fail(O3G_ERR_COMM, "libnccl.so.2 not loadable");
+    nccl_uid uid;
+    memcpy(&uid, id, sizeof(uid));
+    nccl_result_t r = nccl().comm_init_rank(&c->comm, world, uid, rank);
+    if (r != 0) {
+        c->comm = nullptr;
+        c->world = 1;
+        c->rank = 0;
+        return fail(O3G_ERR_COMM, std::string("ncclCommInitRank: ") +
+                                      (nccl().error_string ? nccl().error_string(r) : "?"));
+    }
+    return O3G_OK;
+}
+
+// ---------------------------------------------------------- one-shot
+o3g_status o3g_icp_point_to_plane(const float* source_xyz, int64_t n_source, const float* target_xyz,
+                                  const float* target_normals, int64_t n_target,
+                                  const double init_T[16], double dmax, int32_t max_iterations,
+                                  double relative_fitness, double relative_rmse, double T_out[16],
+                                  double* fitness, double* inlier_rmse, o3g_icp_info* info,
+                                  void* cuda_stream) {
+    static thread_local o3g_ctx* cached[64] = {};
+    if (!init_T || !rigid_ok(init_T)) return fail(O3G_ERR_INVALID_ARGUMENT, "init_T is not a rigid transform");
+    if (!source_xyz) return fail(O3G_ERR_INVALID_ARGUMENT, "source xyz is required");
+    if (n_source <= 0) return fail(O3G_ERR_INVALID_ARGUMENT, "n_source must be > 0");
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    if (dev < 0 || dev >= 64) return fail(O3G_ERR_CUDA, "device index out of range");
+    o3g_ctx*& c = cached[dev];
+    if (!c) TRY(o3g_create(&c, dev, cuda_stream));
+    c->user = (cudaStream_t)cuda_stream;
+    TRY(o3g_set_target(c, target_xyz, target_normals, n_target, dmax));
+    TRY(o3g_set_source(c, source_xyz, n_source, init_T));
+    return o3g_icp_run(c, init_T, max_iterations, relative_fitness, relative_rmse, T_out, fitness,
+                       inlier_rmse, info, nullptr, nullptr);
+}
+
+}  // extern "C"

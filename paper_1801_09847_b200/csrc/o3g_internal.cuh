@@ -1,0 +1,113 @@
+// o3g_internal.cuh — shared declarations of the CUDA library (not installed).
+// Device data layout and kernel entry points; see DESIGN.md §4-§5.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace o3g {
+
+constexpr int kTerms = 29;        // O3G_NTERMS
+constexpr int kTermStride = 32;   // padded per-block / per-rank partial
+constexpr int kK3Threads = 256;   // correspondence kernel block size
+constexpr int kTailThreads = 1024;
+
+// Voxel-hash grid over the target. Cell size
+// h = dmax*(1+2^-20) so the 27-cell stencil provably contains every target
+// within dmax of a query. table index of cell (cx,cy,cz):
+//   dense : (cz*ny + cy)*nx + cx            (collision-free)
+//   hashed: (rowhash(cy,cz) + cx) & hmask   (collisions only add candidates)
+// Along x consecutive cells map to consecutive table entries in both modes,
+// so the 3 cells of one x-row are one contiguous range of the sorted target
+// (two if a hashed row wraps).
+struct GridDev {
+    double ox, oy, oz;   // componentwise min of the target (fp32 values)
+    double inv_h;        // 1 / h
+    int32_t nx, ny, nz;  // cells per axis
+    int32_t hashed;
+    uint32_t hmask;      // table_size - 1 when hashed
+    int32_t pad;
+    int64_t table_size;  // cell_start has table_size + 1 entries
+};
+
+// Loop state, resident in device memory for the whole graph-launched loop.
+struct IcpState {
+    double T[16];
+    double terms[kTermStride];
+    double fit, rmse, fit_prev, rmse_prev;
+    double rel_fit, rel_rmse;
+    double n_total;
+    int32_t it, max_it, passes, done, flags, converged, hist_cap, pad;
+};
+
+enum TailMode : int {
+    TAIL_REDUCE_BLOCKS = 1,  // terms = fixed-order sum of the K3 block partials
+    TAIL_WRITE_RANK = 2,     // store terms into gathered[rank] and stop
+    TAIL_SUM_RANKS = 4,      // terms = sum over gathered[0..world) in rank order
+    TAIL_SOLVE = 8,          // criteria + LDLT + exp + T update (A8)
+    TAIL_STEP = 16,          // store terms only (o3g_icp_step)
+};
+
+__host__ __device__ inline int64_t grid_index_dense(const GridDev& g, int cx, int cy, int cz) {
+    return ((int64_t)cz * g.ny + cy) * (int64_t)g.nx + cx;
+}
+__host__ __device__ inline uint32_t grid_row_hash(int cy, int cz) {
+    return (uint32_t)cy * 0x9E3779B1u ^ (uint32_t)cz * 0x85EBCA77u ^ 0x27D4EB2Fu;
+}
+
+#ifdef __CUDACC__
+// Cell coordinate floor((x - o) / h), computed as floor((x - o) * inv_h) in
+// fp64 without contraction; clamped to [-2, n+1] so far queries cannot
+// overflow (they have no candidates anyway). Used identically for the
+// target points (grid build) and the transformed queries (search).
+__device__ __forceinline__ int cell_coord(double x, double o, double inv_h, int n) {
+    double c = floor(__dmul_rn(__dsub_rn(x, o), inv_h));
+    c = fmin(fmax(c, -2.0), (double)n + 1.0);
+    return (int)c;
+}
+
+// A3: s' = T s, fixed order ((T00 sx + T01 sy) + T02 sz) + T03, no FMA (R2).
+__device__ __forceinline__ void xform_rn(const double* T, float x, float y, float z, double& ox,
+                                         double& oy, double& oz) {
+    const double dx = x, dy = y, dz = z;
+    ox = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(T[0], dx), __dmul_rn(T[1], dy)), __dmul_rn(T[2], dz)), T[3]);
+    oy = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(T[4], dx), __dmul_rn(T[5], dy)), __dmul_rn(T[6], dz)), T[7]);
+    oz = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(T[8], dx), __dmul_rn(T[9], dy)), __dmul_rn(T[10], dz)), T[11]);
+}
+#endif
+
+// ---- launchers (grid_build.cu)
+void launch_bbox(const float* xyz, int64_t n, uint32_t* minmax6, int32_t* nonfinite, int sms,
+                 cudaStream_t s);
+void launch_check_finite(const float* v, int64_t count, int32_t* nonfinite, int sms,
+                         cudaStream_t s);
+void launch_cell_keys(const float* xyz, int64_t n, const GridDev& g, const double* T12_or_null,
+                      uint32_t* keys, int32_t* vals, cudaStream_t s);
+void launch_histogram(const uint32_t* keys, int64_t n, int32_t* counts, cudaStream_t s);
+void launch_gather_target(const float* xyz, const float* nrm, const int32_t* vals_sorted,
+                          const uint32_t* keys_sorted, int64_t n, float4* tpos, float4* tnrm,
+                          unsigned long long* occupied, cudaStream_t s);
+void launch_gather_source(const float* xyz, const int32_t* vals_sorted, int64_t lo, int64_t hi,
+                          float4* out, cudaStream_t s);
+void launch_fill_i32(int32_t* p, int64_t n, int32_t v, cudaStream_t s);
+
+// ---- launchers (icp_kernels.cu)
+struct K3Args {
+    const float4* src;      // sorted local shard (x,y,z, bitcast original index)
+    int32_t n;              // local count
+    const float4* tpos;     // sorted target (x,y,z, bitcast original index)
+    const float4* tnrm;     // sorted target normals (nx,ny,nz,0)
+    const int32_t* cell_start;
+    GridDev g;
+    double r2;              // dmax*dmax (fp64, R1)
+    double dmax, inv_dmax;  // prefilter margin terms
+    const IcpState* st;
+    double* block_partials; // [gridDim.x][kTermStride]
+    int32_t* corr_out;      // original order, nullable
+};
+void launch_k3(const K3Args& a, int blocks, bool prefilter, bool write_corr, cudaStream_t s);
+int k3_max_blocks_per_sm(bool prefilter, bool write_corr);
+void launch_tail(const double* block_partials, int nblocks, double* gathered, int world, int rank,
+                 IcpState* st, double* hist_fit, double* hist_rmse, int mode, cudaStream_t s);
+
+}  // namespace o3g

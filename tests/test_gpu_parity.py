@@ -1,0 +1,345 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Bars (BASELINE.json north_star): correspondence indices bit-exact for the
+same T_in; JTJ / JTr within 1e-9 relative (R14: |a-b| <= 1e-9 max(|b|,
+sum|terms|)); final T within 1e-6 per element; fitness and inlier_rmse
+within 1e-6.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from synth.rng import Stream
+from synth.scenes import rigid, rotation
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+SEARCH = {"exact": 0, "prefilter": 1}
+GRID = {"dense": 1, "hashed": 2}
+
+
+@pytest.fixture(scope="module")
+def o3g():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1801_09847_b200 as m
+    m.lib()
+    return m
+
+
+def _dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a, np.float32)).cuda()
+
+
+def _ctx(o3g, w, search="prefilter", grid="dense", order_T=None, src=None):
+    ctx = o3g.Context(0)
+    ctx.set_option(1, SEARCH[search])
+    ctx.set_option(2, GRID[grid])
+    ctx.set_target(_dev(w["target"]), _dev(w["target_normals"]), w["dmax"])
+    ctx.set_source(_dev(w["source"] if src is None else src), order_T)
+    return ctx
+
+
+def _terms_ok(gpu, ref, rel=1e-9):
+    tol = rel * np.maximum(np.abs(ref["terms"]), ref["abs_terms"]) + 1e-300
+    bad = np.abs(gpu - ref["terms"]) > tol
+    assert not bad.any(), (np.nonzero(bad), gpu[bad], ref["terms"][bad])
+
+
+def _step(ctx, T, n):
+    corr = torch.full((n,), -7, dtype=torch.int32, device="cuda")
+    st = ctx.step(T, corr_out=corr)
+    return corr.cpu().numpy(), st
+
+
+def _perturb(seed, ang=0.01, tr=0.01):
+    rs = Stream(seed)
+    return rigid(rotation(rs.unit_vectors(1)[0], ang), rs.uniform(3, -tr, tr))
+
+
+# -------------------------------------------------------------- golden
+def test_hand_step_golden_gpu(o3g):
+    g = json.load(open(os.path.join(GOLD, "hand_step.json")))
+    for c in g["cases"]:
+        w = dict(source=np.array(c["source"]), target=np.array(c["target"]),
+                 target_normals=np.array(c["normals"]), dmax=c["dmax"])
+        for search in SEARCH:
+            for grid in GRID:
+                with _ctx(o3g, w, search, grid) as ctx:
+                    corr, st = _step(ctx, np.array(c["T"], float), len(c["source"]))
+                    assert corr.tolist() == c["corr"], (c["name"], search, grid)
+                    up = np.array([st["JTJ"][i, j] for i in range(6) for j in range(i, 6)])
+                    assert np.array_equal(up, np.array(c["jtj_upper"], float))
+                    assert np.array_equal(st["JTr"], np.array(c["jtr"], float))
+                    assert st["count"] == c["count"] and st["sum_sq_dist"] == c["sum_sq_dist"]
+
+
+def test_dyadic_nn_golden_gpu(o3g):
+    g = json.load(open(os.path.join(GOLD, "dyadic_nn.json")))
+    for c in g["cases"]:
+        tgt = np.array(c["target"], np.float32)
+        w = dict(source=np.array([c["query"]], np.float32), target=tgt,
+                 target_normals=np.tile([0, 0, 1], (len(tgt), 1)), dmax=c["dmax"])
+        for search in SEARCH:
+            for grid in GRID:
+                with _ctx(o3g, w, search, grid) as ctx:
+                    corr, st = _step(ctx, np.eye(4), 1)
+                    assert corr[0] == c["expect"], (c["name"], search, grid)
+                    if c["expect_d2"] is not None:
+                        assert st["sum_sq_dist"] == c["expect_d2"]
+
+
+def test_adversarial_lattice_ties(o3g):
+    """Dyadic lattice, spacing == dmax, duplicated points at higher indices,
+    queries on the half-lattice: exact ties, d == dmax, shared boundaries."""
+    dmax = 0.25
+    g = np.arange(-4, 5) * 0.25
+    X, Y, Z = np.meshgrid(g, g, g, indexing="ij")
+    tgt = np.stack([X.ravel(), Y.ravel(), Z.ravel()], 1)
+    tgt = np.concatenate([tgt, tgt[::7]]).astype(np.float32)
+    rs = Stream(5)
+    nrm = rs.unit_vectors(len(tgt)).astype(np.float32)
+    qs = np.stack(np.meshgrid(*(np.arange(-9, 10) * 0.125,) * 3, indexing="ij"), -1).reshape(-1, 3)
+    w = dict(source=qs.astype(np.float32), target=tgt, target_normals=nrm, dmax=dmax)
+    ref = oracle.step(np.eye(4), qs, tgt, nrm, dmax, grid=None)
+    for search in SEARCH:
+        for grid in GRID:
+            with _ctx(o3g, w, search, grid) as ctx:
+                corr, st = _step(ctx, np.eye(4), len(qs))
+                assert np.array_equal(corr, ref["corr"]), (search, grid)
+                _terms_ok(st["terms"], ref)
+
+
+def test_ulp_boundary_queries(o3g):
+    """Queries 1 ulp either side of d == dmax and of cell boundaries."""
+    dmax = 0.0625
+    tgt = np.array([[0, 0, 0], [0.0625, 0, 0], [1, 1, 1], [0.125, 0.0625, 0]], np.float32)
+    base = np.float32(0.0625)
+    xs = [np.nextafter(base, np.float32(0)), base, np.nextafter(base, np.float32(1))]
+    q = []
+    for x in xs:
+        q += [[x, 0, 0], [-x, 0, 0], [0, x, 0], [2 * x, 0, 0], [x, x, 0], [0.125 + x, 0.0625, 0]]
+    q = np.array(q, np.float32)
+    nrm = np.tile([0, 0, 1], (4, 1)).astype(np.float32)
+    w = dict(source=q, target=tgt, target_normals=nrm, dmax=dmax)
+    for T in (np.eye(4), rigid(np.eye(3), [2.0 ** -30, -(2.0 ** -28), 0])):
+        ref = oracle.step(T, q, tgt, nrm, dmax, grid=None)
+        for search in SEARCH:
+            with _ctx(o3g, w, search) as ctx:
+                corr, _ = _step(ctx, T, len(q))
+                assert np.array_equal(corr, ref["corr"]), search
+
+
+# -------------------------------------------------------- configs: step
+def _configs(workloads):
+    out = [("tiny", workloads("tiny"), None)]
+    out.append(("depth", workloads("depth"), None))
+    lid = workloads("lidar")
+    out.append(("lidar", lid, Stream(11).integers(4000, len(lid["source"]))))
+    big = workloads("large16m", n=400_000)
+    out.append(("large400k", big, Stream(12).integers(20000, len(big["source"]))))
+    return out
+
+
+@pytest.mark.parametrize("search", list(SEARCH))
+def test_step_parity_configs(o3g, workloads, search):
+    for name, w, subset in _configs(workloads):
+        grid = oracle.Grid(w["target"], w["dmax"])
+        Ts = [w["init_T"], w["T_true"], w["T_true"] @ _perturb(3, 0.003, 0.005)]
+        with _ctx(o3g, w, search, order_T=w["init_T"]) as ctx:
+            for T in Ts:
+                corr, st = _step(ctx, T, len(w["source"]))
+                ref = oracle.step(T, w["source"], w["target"], w["target_normals"], w["dmax"],
+                                  grid=grid, subset=subset)
+                got = corr if subset is None else corr[subset]
+                assert np.array_equal(got, ref["corr"]), (name, search, int((got != ref["corr"]).sum()))
+                if subset is None:
+                    _terms_ok(st["terms"], ref)
+                else:
+                    assert st["count"] == float((corr >= 0).sum())
+                    A = st["JTJ"]
+                    assert np.array_equal(A, A.T)
+                    ev = np.linalg.eigvalsh(A)
+                    assert ev.min() >= -1e-9 * ev.max()
+
+
+def test_hashed_grid_matches_dense(o3g, workloads):
+    w = workloads("depth")
+    T = w["T_true"] @ _perturb(4, 0.01, 0.01)
+    out = {}
+    for grid in GRID:
+        with _ctx(o3g, w, "prefilter", grid) as ctx:
+            out[grid] = _step(ctx, T, len(w["source"]))
+            info = ctx.grid_info()
+            assert info["hashed"] == (grid == "hashed")
+    assert np.array_equal(out["dense"][0], out["hashed"][0])
+    ref = oracle.step(T, w["source"], w["target"], w["target_normals"], w["dmax"])
+    _terms_ok(out["hashed"][1]["terms"], ref)
+
+
+# -------------------------------------------------------- configs: loop
+@pytest.mark.parametrize("name", ["tiny", "depth"])
+def test_loop_parity(o3g, workloads, name):
+    w = workloads(name)
+    ref = oracle.icp(w["source"], w["target"], w["target_normals"], w["dmax"], w["iters"],
+                     init_T=w["init_T"])
+    for search in SEARCH:
+        with _ctx(o3g, w, search, order_T=w["init_T"]) as ctx:
+            r = ctx.run(w["init_T"], w["iters"], history=True)
+        assert np.abs(r.transformation - ref["T"]).max() <= 1e-6, (name, search)
+        assert abs(r.fitness - ref["fitness"]) <= 1e-6
+        assert abs(r.inlier_rmse - ref["inlier_rmse"]) <= 1e-6
+        assert r.iterations == ref["iterations"] and r.converged == ref["converged"]
+        assert r.flags == ref["flags"]
+        n = min(len(r.hist_fitness), len(ref["hist_fitness"]))
+        assert np.abs(r.hist_fitness[:n] - ref["hist_fitness"][:n]).max() <= 1e-6
+
+
+def test_loop_parity_lidar_subsample(o3g, workloads):
+    """LiDAR: ~6.6k candidates per query make the oracle slow; loop parity on
+    a 3000-point source subsample against the full target."""
+    w = workloads("lidar")
+    sub = np.sort(Stream(13).integers(3000, len(w["source"])))
+    src = w["source"][sub]
+    ref = oracle.icp(src, w["target"], w["target_normals"], w["dmax"], 10)
+    with _ctx(o3g, w, "prefilter", src=src) as ctx:
+        r = ctx.run(np.eye(4), 10)
+    assert np.abs(r.transformation - ref["T"]).max() <= 1e-6
+    assert abs(r.fitness - ref["fitness"]) <= 1e-6 and abs(r.inlier_rmse - ref["inlier_rmse"]) <= 1e-6
+
+
+def test_full_loop_recovers_motion_depth(o3g, workloads):
+    w = workloads("depth")
+    with _ctx(o3g, w) as ctx:
+        r = ctx.run(w["init_T"], w["iters"])
+    assert np.abs(r.transformation[:3, 3] - w["T_true"][:3, 3]).max() < 5e-3
+    assert r.fitness > 0.5
+
+
+# -------------------------------------------------------- API / edges
+def test_one_shot_host_and_device_agree(o3g, workloads):
+    w = workloads("tiny")
+    a = o3g.icp_point_to_plane(w["source"], w["target"], w["target_normals"], w["dmax"],
+                               w["init_T"], w["iters"])
+    b = o3g.icp_point_to_plane(_dev(w["source"]), _dev(w["target"]), _dev(w["target_normals"]),
+                               w["dmax"], w["init_T"], w["iters"])
+    assert np.array_equal(a.transformation, b.transformation)
+    assert a.fitness == b.fitness and a.inlier_rmse == b.inlier_rmse
+    with _ctx(o3g, w, order_T=w["init_T"]) as ctx:
+        c = ctx.run(w["init_T"], w["iters"])
+    assert np.array_equal(a.transformation, c.transformation)
+
+
+def test_deterministic(o3g, workloads):
+    w = workloads("depth")
+    with _ctx(o3g, w) as ctx:
+        r1 = ctx.run(w["init_T"], 10)
+        r2 = ctx.run(w["init_T"], 10)
+    assert np.array_equal(r1.transformation, r2.transformation) and r1.fitness == r2.fitness
+
+
+@pytest.mark.parametrize("n", [1, 31, 257, 1025, 100_003])
+def test_ragged_sizes(o3g, workloads, n):
+    w = workloads("depth")
+    src = np.concatenate([w["source"], w["source"] + np.float32(0.003)])[:n]
+    T = w["T_true"]
+    sub = None if n <= 2000 else np.arange(0, n, 37)
+    with _ctx(o3g, w, src=src) as ctx:
+        corr, st = _step(ctx, T, n)
+    ref = oracle.step(T, src, w["target"], w["target_normals"], w["dmax"],
+                      grid=oracle.Grid(w["target"], w["dmax"]), subset=sub)
+    assert np.array_equal(corr if sub is None else corr[sub], ref["corr"])
+    if sub is None:
+        _terms_ok(st["terms"], ref)
+
+
+def test_invalid_arguments(o3g, workloads):
+    w = workloads("tiny")
+    E = o3g.InvalidArgument
+    with pytest.raises(E):
+        o3g.icp_point_to_plane(np.zeros((0, 3)), w["target"], w["target_normals"], 0.05)
+    with pytest.raises(E):
+        o3g.icp_point_to_plane(w["source"], w["target"], w["target_normals"], 0.0)
+    with pytest.raises(E):
+        o3g.icp_point_to_plane(w["source"], w["target"], w["target_normals"], float("nan"))
+    bad = w["source"].copy()
+    bad[17, 1] = np.inf
+    with pytest.raises(E):
+        o3g.icp_point_to_plane(bad, w["target"], w["target_normals"], 0.05)
+    badn = w["target_normals"].copy()
+    badn[3, 0] = np.nan
+    with pytest.raises(E):
+        o3g.icp_point_to_plane(w["source"], w["target"], badn, 0.05)
+    T = np.eye(4)
+    T[0, 0] = 1.1
+    with pytest.raises(E):
+        o3g.icp_point_to_plane(w["source"], w["target"], w["target_normals"], 0.05, init=T)
+    with pytest.raises(E):
+        o3g.icp_point_to_plane(w["source"], w["target"], w["target_normals"], 0.05, max_iterations=-1)
+    with pytest.raises(E):
+        o3g.icp_point_to_plane(w["source"], w["target"], w["target_normals"], 0.05, relative_rmse=-1)
+    with pytest.raises(E):
+        o3g.icp_point_to_plane(w["source"], w["target"], None, 0.05)
+
+
+def test_flags_no_corr_and_degenerate(o3g, workloads):
+    w = workloads("tiny")
+    far = w["source"] + np.float32(100.0)
+    r = o3g.icp_point_to_plane(far, w["target"], w["target_normals"], 0.05, max_iterations=5)
+    assert r.flags & o3g.FLAG_NO_CORRESPONDENCES and r.fitness == 0 and r.inlier_rmse == 0
+    assert np.array_equal(r.transformation, np.eye(4)) and r.iterations == 0
+    rs = Stream(3)
+    tgt = rs.uniform(15, -1, 1).reshape(5, 3).astype(np.float32)
+    r = o3g.icp_point_to_plane(tgt, tgt, rs.unit_vectors(5), 0.1, max_iterations=5)
+    ref = oracle.icp(tgt, tgt, rs.unit_vectors(5), 0.1, 5)
+    assert r.flags == ref["flags"] == oracle.FLAG_DEGENERATE and r.iterations == 0
+    # the tiny scene with source = target is exactly degenerate (yaw column of J is 0)
+    r = o3g.icp_point_to_plane(w["target"], w["target"], w["target_normals"], 0.05)
+    assert r.flags == o3g.FLAG_DEGENERATE and r.fitness == 1.0
+
+
+def test_zero_iterations_and_criteria_semantics(o3g, workloads):
+    w = workloads("tiny")
+    for K, ef in ((0, 1e-6), (7, 0.0), (7, np.inf)):
+        ref = oracle.icp(w["source"], w["target"], w["target_normals"], w["dmax"], K,
+                         relative_fitness=ef, relative_rmse=ef)
+        r = o3g.icp_point_to_plane(w["source"], w["target"], w["target_normals"], w["dmax"],
+                                   max_iterations=K, relative_fitness=ef, relative_rmse=ef)
+        assert r.iterations == ref["iterations"] and r.passes == ref["passes"]
+        assert abs(r.fitness - ref["fitness"]) <= 1e-12
+
+
+def test_kernel_timing_and_launch_count(o3g, workloads):
+    w = workloads("depth")
+    with _ctx(o3g, w) as ctx:
+        ctx.set_option(3, 1)
+        before = ctx.launch_count()
+        r = ctx.run(w["init_T"], 5, 0.0, 0.0)
+        k3_ms, k3_n, tail_ms = ctx.last_run_kernel_ms()
+        assert k3_n == r.passes == 6 and k3_ms > 0
+        assert ctx.launch_count() - before == 2 * 6
+
+
+# -------------------------------------------------- full-size (bench) config
+@pytest.mark.slow
+def test_large16m_full_size_sampled(o3g, workloads):
+    """BASELINE config 5 at full size in the bench's launch configuration:
+    sampled correspondences vs the oracle's grid, plus invariants."""
+    w = workloads("large16m")
+    sub = Stream(14).integers(20000, len(w["source"]))
+    grid = oracle.Grid(w["target"], w["dmax"])
+    with _ctx(o3g, w, order_T=w["init_T"]) as ctx:
+        for T in (w["init_T"], w["T_true"]):
+            corr, st = _step(ctx, T, len(w["source"]))
+            ref = oracle.step(T, w["source"], w["target"], w["target_normals"], w["dmax"],
+                              grid=grid, subset=sub)
+            assert np.array_equal(corr[sub], ref["corr"])
+            assert st["count"] == float((corr >= 0).sum())
+            assert corr.max() < len(w["target"]) and corr.min() >= -1
+        r = ctx.run(w["init_T"], 30, 0.0, 0.0)
+    assert np.abs(r.transformation - w["T_true"]).max() < 1e-2

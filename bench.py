@@ -44,7 +44,7 @@ def parse():
     ap.add_argument("--impl", default="o3g", choices=["o3g", "reference"])
     ap.add_argument("--config", default="large16m")
     ap.add_argument("--iters", type=int, default=None)
-    ap.add_argument("--search", type=int, default=1, help="0 exact fp64 scan, 1 fp32 prefilter")
+    ap.add_argument("--search", type=int, default=1, help="K3 variant: 0 exact fp64 scan, 1 two-pass warp (default), 2 single-pass prefilter, 3 tile-sorted two-pass")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--n", type=int, default=None, help="override point count (testing only)")
@@ -297,7 +297,7 @@ def main():
             "config": {"workload": a.config, "n_source": n, "n_target": m, "dmax": w["dmax"],
                        "iterations": iters, "updates_per_step": updates,
                        "parallelism": f"source-shard x{world}, target grid replicated",
-                       "search": ["exact-fp64", "fp32-prefilter+exact-fp64"][a.search],
+                       "search": ["exact-fp64", "two-pass fp32-prefilter+exact-fp64", "single-pass fp32-prefilter+exact-fp64", "tile-sorted two-pass fp32-prefilter+exact-fp64"][a.search],
                        "l2": "inputs 576 MB > 126 MB L2 (no flush needed)" if a.config == "large16m"
                              else "inputs resident; L2-resident working set"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",

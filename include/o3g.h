@@ -148,15 +148,21 @@ o3g_status o3g_nccl_unique_id(void* id_out_128);
 o3g_status o3g_dist_init(o3g_ctx* ctx, int rank, int world, const void* nccl_unique_id_128);
 
 /* -------------------------------------------------------------- options
- * O3G_OPT_SEARCH: 0 = exact fp64 scan of every candidate, 1 = fp32
- *   prefilter with a proven margin + exact fp64 decision (default). Both
- *   give bit-identical correspondences.
+ * O3G_OPT_SEARCH: correspondence-kernel variant, all bit-identical
+ *   (DESIGN.md §5): 0 = exact fp64 test of every candidate; 1 = two-pass
+ *   warp kernel (fp32 prefilter with a proven margin + exact fp64 decision);
+ *   2 = single-pass fp32 prefilter + exact decision; 3 = two-pass kernel on
+ *   count-sorted 128-query tiles (default).
  * O3G_OPT_GRID: 0 = auto, 1 = force dense cell table, 2 = force hashed
  *   cell table (collisions only add candidates; results are identical).
  * O3G_OPT_TIMING: 1 = record CUDA events around every correspondence
  *   kernel inside the run graph (read with o3g_last_run_kernel_ms).
- * O3G_OPT_BLOCKS_PER_SM: override the persistent grid size (0 = auto).  */
-enum { O3G_OPT_SEARCH = 1, O3G_OPT_GRID = 2, O3G_OPT_TIMING = 3, O3G_OPT_BLOCKS_PER_SM = 4 };
+ * O3G_OPT_BLOCKS_PER_SM: override the persistent grid size (0 = auto).
+ * O3G_OPT_NBR_MASK: 1 = skip queries whose 27-cell stencil is empty using a
+ *   dilated occupancy bitmap of the dense grid (default), 0 = off. Results
+ *   are identical either way.                                            */
+enum { O3G_OPT_SEARCH = 1, O3G_OPT_GRID = 2, O3G_OPT_TIMING = 3, O3G_OPT_BLOCKS_PER_SM = 4,
+       O3G_OPT_NBR_MASK = 5 };
 o3g_status o3g_set_option(o3g_ctx* ctx, int option, int64_t value);
 
 /* Sum of the correspondence-kernel (K3) durations of the last o3g_icp_run

@@ -120,6 +120,34 @@ __global__ void k_fill_i32(int32_t* p, int64_t n, int32_t v) {
         p[i] = v;
 }
 
+__global__ void k_occupancy_bits(const int32_t* __restrict__ cs, int64_t ncells,
+                                 uint32_t* __restrict__ bits) {
+    const int64_t nw = (ncells + 31) / 32;
+    for (int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; w < nw;
+         w += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int64_t k = w * 32 + (threadIdx.x & 31);
+        const bool occ = k < ncells && cs[k + 1] > cs[k];
+        const uint32_t b = __ballot_sync(0xffffffffu, occ);
+        if ((threadIdx.x & 31) == 0) bits[w] = b;
+    }
+}
+
+// 32 bits of `in` starting at bit position `pos` (zeros outside [0, nbits))
+__device__ __forceinline__ uint32_t bits_at(const uint32_t* in, int64_t nw, int64_t pos) {
+    const int64_t wi = pos >= 0 ? pos / 32 : -((-pos + 31) / 32);
+    const int sh = (int)(pos - wi * 32);
+    const uint32_t lo = (wi >= 0 && wi < nw) ? in[wi] : 0u;
+    const uint32_t hi = (wi + 1 >= 0 && wi + 1 < nw) ? in[wi + 1] : 0u;
+    return __funnelshift_r(lo, hi, sh);
+}
+
+__global__ void k_dilate_bits(const uint32_t* __restrict__ in, uint32_t* __restrict__ out,
+                              int64_t nw, int64_t off) {
+    for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < nw;
+         w += (int64_t)gridDim.x * blockDim.x)
+        out[w] = in[w] | bits_at(in, nw, w * 32 - off) | bits_at(in, nw, w * 32 + off);
+}
+
 static int blocks_for(int64_t n, int threads, int cap = 148 * 16) {
     int64_t b = (n + threads - 1) / threads;
     if (b < 1) b = 1;
@@ -154,6 +182,16 @@ void launch_gather_source(const float* xyz, const int32_t* vals, int64_t lo, int
                           float4* out, cudaStream_t s) {
     k_gather_source<<<blocks_for(hi - lo, 256), 256, 0, s>>>(xyz, vals, lo, hi, out);
 }
+void launch_nbr_bits(const int32_t* cs, int64_t ncells, int64_t nx, int64_t nxny, uint32_t* tmp,
+                     uint32_t* out, cudaStream_t s) {
+    const int64_t nw = (ncells + 31) / 32;
+    k_occupancy_bits<<<blocks_for(nw * 32, 256), 256, 0, s>>>(cs, ncells, out);
+    k_dilate_bits<<<blocks_for(nw, 256), 256, 0, s>>>(out, tmp, nw, 1);
+    k_dilate_bits<<<blocks_for(nw, 256), 256, 0, s>>>(tmp, out, nw, nx);
+    k_dilate_bits<<<blocks_for(nw, 256), 256, 0, s>>>(out, tmp, nw, nxny);
+    cudaMemcpyAsync(out, tmp, nw * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s);
+}
+
 void launch_fill_i32(int32_t* p, int64_t n, int32_t v, cudaStream_t s) {
     k_fill_i32<<<blocks_for(n, 256), 256, 0, s>>>(p, n, v);
 }

@@ -12,23 +12,11 @@
 #include <float.h>
 #include <math_constants.h>
 
-#include "o3g_internal.cuh"
+#include "k3_common.cuh"
 
 namespace o3g {
 
 // ------------------------------------------------------------------- K3
-// Prefilter threshold. For a query s' (fp64) let
-// sh = fl32(s') and E1 >= ||s' - sh||_1 (1 + 2^-20). Every candidate whose
-// exact fp64 distance d2_64 <= B satisfies
-//   df = fl32(|t - sh|^2) <= (1+2^-20) (B (1+2^-20) + E1 (B/dmax + dmax) + E1^2)
-// (AM-GM bounds 2 sqrt(B) by B/dmax + dmax), so rejecting df > thr never
-// drops a candidate that could win or tie under the exact fp64 rule.
-__device__ __forceinline__ float prefilter_thr(double B, double E1, double dmax, double inv_dmax) {
-    const double k = 1.0 + 9.5367431640625e-07;  // 1 + 2^-20
-    double v = B * k + E1 * (B * inv_dmax + dmax) + E1 * E1;
-    return __double2float_ru(v * k);
-}
-
 template <bool PREFILTER, bool WRITE_CORR>
 __global__ void __launch_bounds__(kK3Threads) k3_corr_reduce(const K3Args a) {
     __shared__ double sT[12];
@@ -153,6 +141,238 @@ __global__ void __launch_bounds__(kK3Threads) k3_corr_reduce(const K3Args a) {
     }
 }
 
+// ------------------------------------------------------------ K3 (v2)
+// k3_balanced: same contract and bit-identical results as k3_corr_reduce,
+// organised for SIMT efficiency:
+//  * setup: each lane stages its query's non-empty x-row ranges in smem;
+//  * pass 1: ONE merged loop over all of the lane's candidates, branch-free
+//    fp32 body tracking the smallest prefilter value m1 (at j1) and the
+//    smallest over all other candidates m2;
+//  * decision: exact fp64 d2 of j1; if m2 > thr(min(d2, r2)) no other
+//    candidate can win or tie (§5.2), else a rare exact filtered rescan;
+//  * accumulation (A5/A6): the warp's 32 records form V (32x8: J, r, m) and
+//    W (32x8: J, m, d2); C += V^T W is a dense 8x8x32 contraction, done on
+//    the fp64 tensor cores (mma.sync m8n8k4 f64, 8 per batch, skipped for
+//    record groups with no match). C holds JTJ (C[a][b]), JTr (C[6][b]),
+//    the count (C[7][6] = sum m*m) and sum d2 (C[7][7] = sum m*d2). Two fp64
+//    accumulators per lane instead of 29, so occupancy is not
+//    register-bound, and the order of every sum is fixed.
+__host__ __device__ inline int k3v2_slots(int hashed) { return hashed ? 18 : 9; }
+// per-warp smem: the segment list (setup .. decision) and, aliased on it, the
+// 9-row record staging J0..J5, r, m, d2 (accumulation), each row kVW doubles
+__host__ __device__ inline size_t k3v2_warp_bytes(int hashed) {
+    const size_t a = 32 * k3v2_slots(hashed) * sizeof(int2), b = 9 * kVW * sizeof(double);
+    return a > b ? a : b;
+}
+inline size_t k3v2_smem(int hashed) { return (size_t)(kK3Threads / 32) * k3v2_warp_bytes(hashed); }
+
+template <bool WRITE_CORR>
+__global__ void __launch_bounds__(kK3Threads, 4) k3_balanced(const K3Args a) {
+    extern __shared__ __align__(16) unsigned char k3smem[];
+    __shared__ double sT[12];
+    __shared__ double red[kK3Threads / 32][64];
+    if (a.st->done) return;
+    if (threadIdx.x < 12) sT[threadIdx.x] = a.st->T[threadIdx.x];
+    __syncthreads();
+
+    const GridDev g = a.g;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int S = k3v2_slots(g.hashed);
+    int2* segs = (int2*)(k3smem + (size_t)warp * k3v2_warp_bytes(g.hashed));
+    double* vw = (double*)segs;   // [9 rows][kVW], aliases segs (used after the decision)
+    double acc0 = 0.0, acc1 = 0.0;           // C[lane>>2][2(lane&3)+{0,1}]
+    const double r2 = a.r2;
+
+    const int gw = blockIdx.x * (kK3Threads / 32) + warp;
+    const int nw = gridDim.x * (kK3Threads / 32);
+    const int* __restrict__ cs = a.cell_start;
+    const int nxny = g.nx * g.ny;
+    for (int base = gw * 32; base < a.n; base += nw * 32) {
+        const int i = base + lane;
+        double sx = 0.0, sy = 0.0, sz = 0.0, E1 = 0.0;
+        float shx = 0.f, shy = 0.f, shz = 0.f, thr0 = 0.f;
+        int nseg = 0, c = 0;
+        float4 p = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (i < a.n) {
+            p = __ldg(&a.src[i]);
+            xform_rn(sT, p.x, p.y, p.z, sx, sy, sz);
+            const int cx = cell_coord(sx, g.ox, g.inv_h, g.nx);
+            const int cy = cell_coord(sy, g.oy, g.inv_h, g.ny);
+            const int cz = cell_coord(sz, g.oz, g.inv_h, g.nz);
+            const int xlo = max(cx - 1, 0), xhi = min(cx + 1, g.nx - 1);
+            const int ylo = max(cy - 1, 0), yhi = min(cy + 1, g.ny - 1);
+            const int zlo = max(cz - 1, 0), zhi = min(cz + 1, g.nz - 1);
+            bool near = xlo <= xhi && ylo <= yhi && zlo <= zhi;
+            if (near && a.nbr_bits) {
+                // dilated occupancy bitmap: skip queries with no occupied neighbour cell
+                const int kc = (min(max(cz, 0), g.nz - 1) * g.ny + min(max(cy, 0), g.ny - 1)) * g.nx +
+                               min(max(cx, 0), g.nx - 1);
+                near = (__ldg(&a.nbr_bits[kc >> 5]) >> (kc & 31)) & 1u;
+            }
+            if (!g.hashed && near) {
+                // dense table: all 18 row-boundary loads issued back to back;
+                // 32-bit row indices (table_size < 2^31)
+                const int w = xhi - xlo + 1;
+                const int rb0 = ((cz - 1) * g.ny + (cy - 1)) * g.nx + xlo;
+                int bb[9], ee[9];
+#pragma unroll
+                for (int r = 0; r < 9; ++r) {
+                    const int z = cz + r / 3 - 1, y = cy + r % 3 - 1;
+                    const bool ok = z >= zlo && z <= zhi && y >= ylo && y <= yhi;
+                    const int rb = rb0 + (r / 3) * nxny + (r % 3) * g.nx;
+                    bb[r] = ok ? __ldg(cs + rb) : 0;
+                    ee[r] = ok ? __ldg(cs + rb + w) : 0;
+                }
+#pragma unroll
+                for (int r = 0; r < 9; ++r) {
+                    if (ee[r] > bb[r]) {
+                        segs[nseg * 32 + lane] = make_int2(bb[r], ee[r]);
+                        ++nseg;
+                        c += ee[r] - bb[r];
+                    }
+                }
+            } else if (g.hashed && near) {
+                for (int z = zlo; z <= zhi; ++z) {
+                    for (int y = ylo; y <= yhi; ++y) {
+                        int b0, e0, b1 = 0, e1 = 0;
+                        if (!g.hashed) {
+                            const int rb = (z * g.ny + y) * g.nx;   // < table_size < 2^31
+                            b0 = __ldg(&a.cell_start[rb + xlo]);
+                            e0 = __ldg(&a.cell_start[rb + xhi + 1]);
+                        } else {
+                            const uint32_t s0 = (grid_row_hash(y, z) + (uint32_t)xlo) & g.hmask;
+                            const uint32_t cnt = (uint32_t)(xhi - xlo + 1);
+                            b0 = __ldg(&a.cell_start[s0]);
+                            if ((uint64_t)s0 + cnt <= (uint64_t)g.hmask + 1) {
+                                e0 = __ldg(&a.cell_start[s0 + cnt]);
+                            } else {
+                                e0 = __ldg(&a.cell_start[(int64_t)g.hmask + 1]);
+                                b1 = __ldg(&a.cell_start[0]);
+                                e1 = __ldg(&a.cell_start[(s0 + cnt) & g.hmask]);
+                            }
+                        }
+                        if (e0 > b0) { segs[nseg * 32 + lane] = make_int2(b0, e0); ++nseg; c += e0 - b0; }
+                        if (e1 > b1) { segs[nseg * 32 + lane] = make_int2(b1, e1); ++nseg; c += e1 - b1; }
+                    }
+                }
+            }
+            if (c > 0) {
+                shx = __double2float_rn(sx);
+                shy = __double2float_rn(sy);
+                shz = __double2float_rn(sz);
+                E1 = (fabs(sx - (double)shx) + fabs(sy - (double)shy) + fabs(sz - (double)shz)) *
+                     (1.0 + 9.5367431640625e-07);
+                thr0 = prefilter_thr(r2, E1, a.dmax, a.inv_dmax);
+            }
+        }
+
+        // pass 1: branch-free fp32 scan of every candidate of this lane's query
+        float m1 = CUDART_INF_F, m2 = CUDART_INF_F;
+        int j1 = -1;
+        {
+            int k = 0;
+            int2 sg = c > 0 ? segs[lane] : make_int2(0, 0);
+            int j = sg.x, e = sg.y;
+            for (int it = 0; it < c; ++it) {
+                if (j == e) {
+                    ++k;
+                    sg = segs[k * 32 + lane];
+                    j = sg.x, e = sg.y;
+                }
+                const float4 t = __ldg(&a.tpos[j]);
+                const float ux = t.x - shx, uy = t.y - shy, uz = t.z - shz;
+                const float df = fmaf(uz, uz, fmaf(uy, uy, ux * ux));
+                const bool lt = df < m1;
+                m2 = fminf(m2, lt ? m1 : df);
+                m1 = lt ? df : m1;
+                j1 = lt ? j : j1;
+                ++j;
+            }
+        }
+
+        // decision (exact fp64 rule, R1-R3)
+        int win = -1, widx = -1;
+        double wd2 = 0.0;
+        float4 wq = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (c > 0 && m1 <= thr0) {
+            const float4 t = __ldg(&a.tpos[j1]);
+            const double dx = __dsub_rn(sx, (double)t.x), dy = __dsub_rn(sy, (double)t.y),
+                         dz = __dsub_rn(sz, (double)t.z);
+            const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+            const double B = d2 <= r2 ? d2 : r2;
+            if (m2 > prefilter_thr(B, E1, a.dmax, a.inv_dmax)) {
+                if (d2 <= r2) { win = j1, widx = __float_as_int(t.w), wd2 = d2, wq = t; }
+            } else {
+                // near-tie (or duplicate visit): exact filtered rescan
+                double bd = CUDART_INF;
+                int bidx = INT_MAX;
+                float thr = thr0;
+                for (int k = 0; k < nseg; ++k) {
+                    const int2 sg = segs[k * 32 + lane];
+                    for (int j = sg.x; j < sg.y; ++j) {
+                        const float4 u = __ldg(&a.tpos[j]);
+                        const float ux = u.x - shx, uy = u.y - shy, uz = u.z - shz;
+                        if (fmaf(uz, uz, fmaf(uy, uy, ux * ux)) > thr) continue;
+                        const double ex = __dsub_rn(sx, (double)u.x), ey = __dsub_rn(sy, (double)u.y),
+                                     ez = __dsub_rn(sz, (double)u.z);
+                        const double e2 = __dadd_rn(__dadd_rn(__dmul_rn(ex, ex), __dmul_rn(ey, ey)),
+                                                    __dmul_rn(ez, ez));
+                        const int idx = __float_as_int(u.w);
+                        if (e2 <= r2 && (e2 < bd || (e2 == bd && idx < bidx))) {
+                            bd = e2, bidx = idx, win = j, wq = u;
+                            thr = prefilter_thr(bd, E1, a.dmax, a.inv_dmax);
+                        }
+                    }
+                }
+                if (win >= 0) widx = bidx, wd2 = bd;
+            }
+        }
+        if (WRITE_CORR && i < a.n) a.corr_out[__float_as_int(p.w)] = widx;
+
+        // A5: r = (s'-q).n, J = [s' x n ; n] (R4) -> V = (J, r, m), W = (J, m, d2)
+        const unsigned matched = __ballot_sync(0xffffffffu, win >= 0);
+        if (matched) {
+            double v[8] = {0, 0, 0, 0, 0, 0, 0, 0}, d2w = 0.0;
+            if (win >= 0) {
+                const float4 nf = __ldg(&a.tnrm[win]);
+                const double nx = nf.x, ny = nf.y, nz = nf.z;
+                v[0] = sy * nz - sz * ny;
+                v[1] = sz * nx - sx * nz;
+                v[2] = sx * ny - sy * nx;
+                v[3] = nx, v[4] = ny, v[5] = nz;
+                v[6] = (sx - (double)wq.x) * nx + (sy - (double)wq.y) * ny + (sz - (double)wq.z) * nz;
+                v[7] = 1.0;
+                d2w = wd2;
+            }
+#pragma unroll
+            for (int q = 0; q < 8; ++q) vw[q * kVW + lane] = v[q];
+            vw[8 * kVW + lane] = d2w;
+            __syncwarp();
+            // A6: C += V^T W over the 32 records, 4 records per mma (fixed order)
+            // V rows (J0..J5, r, m) = 0..7; W rows (J0..J5, m, d2) = 0..5, 7, 8
+            const int row = lane >> 2, kk = lane & 3, wrow = row < 6 ? row : row + 1;
+#pragma unroll
+            for (int c4 = 0; c4 < 8; ++c4) {
+                if ((matched >> (4 * c4)) & 0xFu)
+                    dmma884(acc0, acc1, vw[row * kVW + 4 * c4 + kk], vw[wrow * kVW + 4 * c4 + kk]);
+            }
+            __syncwarp();
+        }
+    }
+
+    red[warp][(lane >> 2) * 8 + 2 * (lane & 3)] = acc0;
+    red[warp][(lane >> 2) * 8 + 2 * (lane & 3) + 1] = acc1;
+    __syncthreads();
+    if (threadIdx.x < kTermStride) {
+        double s = 0.0;
+        if (threadIdx.x < kTerms) {
+            const int ci = term_cidx(threadIdx.x);
+            for (int w = 0; w < kK3Threads / 32; ++w) s += red[w][ci];
+        }
+        a.block_partials[(size_t)blockIdx.x * kTermStride + threadIdx.x] = s;
+    }
+}
+
 template <bool P, bool W>
 static int occ_of() {
     int b = 0;
@@ -160,18 +380,46 @@ static int occ_of() {
     return b;
 }
 
-int k3_max_blocks_per_sm(bool prefilter, bool write_corr) {
-    if (prefilter) return write_corr ? occ_of<true, true>() : occ_of<true, false>();
-    return write_corr ? occ_of<false, true>() : occ_of<false, false>();
+template <bool W>
+static int occ_v2(int hashed) {
+    static bool attr_done[2] = {false, false};
+    if (!attr_done[hashed]) {
+        cudaFuncSetAttribute(k3_balanced<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)k3v2_smem(1));
+        attr_done[hashed] = true;
+    }
+    int b = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k3_balanced<W>, kK3Threads, k3v2_smem(hashed));
+    return b;
 }
 
-void launch_k3(const K3Args& a, int blocks, bool prefilter, bool write_corr, cudaStream_t s) {
-    if (prefilter) {
-        if (write_corr) k3_corr_reduce<true, true><<<blocks, kK3Threads, 0, s>>>(a);
-        else k3_corr_reduce<true, false><<<blocks, kK3Threads, 0, s>>>(a);
-    } else {
-        if (write_corr) k3_corr_reduce<false, true><<<blocks, kK3Threads, 0, s>>>(a);
-        else k3_corr_reduce<false, false><<<blocks, kK3Threads, 0, s>>>(a);
+int k3_max_blocks_per_sm(int variant, bool write_corr, int hashed) {
+    switch (variant) {
+        case 0: return write_corr ? occ_of<false, true>() : occ_of<false, false>();
+        case 2: return write_corr ? occ_of<true, true>() : occ_of<true, false>();
+        case 3: return k3_sorted_blocks_per_sm(write_corr, hashed);
+        default: return write_corr ? occ_v2<true>(hashed) : occ_v2<false>(hashed);
+    }
+}
+
+void launch_k3(const K3Args& a, int blocks, int variant, bool write_corr, cudaStream_t s) {
+    switch (variant) {
+        case 0:
+            if (write_corr) k3_corr_reduce<false, true><<<blocks, kK3Threads, 0, s>>>(a);
+            else k3_corr_reduce<false, false><<<blocks, kK3Threads, 0, s>>>(a);
+            break;
+        case 2:
+            if (write_corr) k3_corr_reduce<true, true><<<blocks, kK3Threads, 0, s>>>(a);
+            else k3_corr_reduce<true, false><<<blocks, kK3Threads, 0, s>>>(a);
+            break;
+        case 3: launch_k3_sorted(a, blocks, write_corr, s); break;
+        default: {
+            const size_t sm = k3v2_smem(a.g.hashed);
+            occ_v2<true>(a.g.hashed);
+            occ_v2<false>(a.g.hashed);
+            if (write_corr) k3_balanced<true><<<blocks, kK3Threads, sm, s>>>(a);
+            else k3_balanced<false><<<blocks, kK3Threads, sm, s>>>(a);
+        }
     }
 }
 

@@ -119,14 +119,15 @@ struct o3g_ctx {
     cudaEvent_t fence = nullptr;
 
     // options
-    int search = 1, grid_mode = 0, timing = 0, bps_override = 0;
+    int search = 1, grid_mode = 0, timing = 0, bps_override = 0, nbr_mask = 1;
 
     // target grid
     int64_t m = 0;
     double dmax = 0.0;
     GridDev g{};
     int64_t occupied = 0;
-    DevBuf tpos, tnrm, cell_start, counts;
+    DevBuf tpos, tnrm, cell_start, counts, nbr_a, nbr_b;
+    bool nbr_ready = false;
     // scratch
     DevBuf keys_a, keys_b, vals_a, vals_b, cub_tmp, stage_a, stage_b, misc;
     // source
@@ -279,7 +280,7 @@ o3g_status o3g_destroy(o3g_ctx* c) {
     if (c->exec) cudaStreamSynchronize(c->exec);
     invalidate_graph(c);
     for (auto ev : c->events) cudaEventDestroy(ev);
-    DevBuf* bufs[] = {&c->tpos, &c->tnrm, &c->cell_start, &c->counts, &c->keys_a, &c->keys_b,
+    DevBuf* bufs[] = {&c->tpos, &c->tnrm, &c->cell_start, &c->counts, &c->nbr_a, &c->nbr_b, &c->keys_a, &c->keys_b,
                       &c->vals_a, &c->vals_b, &c->cub_tmp, &c->stage_a, &c->stage_b, &c->misc,
                       &c->src4, &c->partials, &c->gathered, &c->state, &c->hist_fit, &c->hist_rmse};
     for (DevBuf* b : bufs) b->release();
@@ -295,7 +296,7 @@ o3g_status o3g_set_option(o3g_ctx* c, int option, int64_t value) {
     if (!c) return fail(O3G_ERR_INVALID_ARGUMENT, "ctx is NULL");
     switch (option) {
         case O3G_OPT_SEARCH:
-            if (value < 0 || value > 1) return fail(O3G_ERR_INVALID_ARGUMENT, "search must be 0 or 1");
+            if (value < 0 || value > 3) return fail(O3G_ERR_INVALID_ARGUMENT, "search must be 0, 1, 2 or 3");
             c->search = (int)value;
             break;
         case O3G_OPT_GRID:
@@ -303,6 +304,7 @@ o3g_status o3g_set_option(o3g_ctx* c, int option, int64_t value) {
             c->grid_mode = (int)value;
             break;
         case O3G_OPT_TIMING: c->timing = value ? 1 : 0; break;
+        case O3G_OPT_NBR_MASK: c->nbr_mask = value ? 1 : 0; break;
         case O3G_OPT_BLOCKS_PER_SM:
             if (value < 0 || value > 64) return fail(O3G_ERR_INVALID_ARGUMENT, "blocks per SM out of range");
             c->bps_override = (int)value;
@@ -393,6 +395,16 @@ o3g_status o3g_set_target(o3g_ctx* c, const float* xyz, const float* normals, in
     launch_gather_target(dx, dn, c->vals_b.as<int32_t>(), c->keys_b.as<uint32_t>(), n,
                          c->tpos.as<float4>(), c->tnrm.as<float4>(), occ, c->exec);
     c->launches += 3;
+    c->nbr_ready = false;
+    if (!g.hashed) {
+        const int64_t nw = (g.table_size + 31) / 32;
+        TRY(c->nbr_a.ensure(nw * 4));
+        TRY(c->nbr_b.ensure(nw * 4));
+        launch_nbr_bits(c->cell_start.as<int32_t>(), g.table_size, g.nx, (int64_t)g.nx * g.ny,
+                        c->nbr_b.as<uint32_t>(), c->nbr_a.as<uint32_t>(), c->exec);
+        c->launches += 4;
+        c->nbr_ready = true;
+    }
     unsigned long long h_occ = 0;
     CK(cudaMemcpyAsync(&h_occ, occ, 8, cudaMemcpyDeviceToHost, c->exec));
     CK(cudaStreamSynchronize(c->exec));
@@ -446,10 +458,11 @@ o3g_status o3g_set_source(o3g_ctx* c, const float* xyz, int64_t n, const double 
     return O3G_OK;
 }
 
-static int k3_blocks(o3g_ctx* c, bool prefilter, bool write_corr) {
-    int bps = c->bps_override ? c->bps_override : k3_max_blocks_per_sm(prefilter, write_corr);
+static int k3_blocks(o3g_ctx* c, bool write_corr) {
+    int bps = c->bps_override ? c->bps_override : k3_max_blocks_per_sm(c->search, write_corr, c->g.hashed);
     if (bps < 1) bps = 1;
-    int64_t need = (c->n_local + kK3Threads - 1) / kK3Threads;
+    const int tpb = k3_threads(c->search);
+    int64_t need = (c->n_local + tpb - 1) / tpb;
     int64_t b = (int64_t)c->sms * bps;
     if (need < b) b = need;
     return (int)(b < 1 ? 1 : b);
@@ -478,16 +491,16 @@ static K3Args k3_args(o3g_ctx* c, int32_t* corr) {
     a.st = c->state.as<IcpState>();
     a.block_partials = c->partials.as<double>();
     a.corr_out = corr;
+    a.nbr_bits = (c->nbr_mask && c->nbr_ready) ? c->nbr_a.as<uint32_t>() : nullptr;
     return a;
 }
 
 // One pass: K3, then the tail (with the rank exchange when distributed).
 static o3g_status enqueue_pass(o3g_ctx* c, int blocks, bool write_corr, int32_t* corr,
                                int tail_mode, cudaEvent_t ev0, cudaEvent_t ev1, int* nlaunch) {
-    const bool prefilter = c->search == 1;
     if (ev0) CK(cudaEventRecordWithFlags(ev0, c->exec, cudaEventRecordExternal));
     if (c->n_local > 0) {
-        launch_k3(k3_args(c, corr), blocks, prefilter, write_corr, c->exec);
+        launch_k3(k3_args(c, corr), blocks, c->search, write_corr, c->exec);
         ++*nlaunch;
     }
     if (ev1) CK(cudaEventRecordWithFlags(ev1, c->exec, cudaEventRecordExternal));
@@ -532,7 +545,7 @@ o3g_status o3g_icp_step(o3g_ctx* c, const double T_in[16], int32_t* corr_out, do
     if (corr_out && !is_device_ptr(corr_out)) return fail(O3G_ERR_INVALID_ARGUMENT, "corr_out must be device memory");
     TRY(enter(c));
     const bool wc = corr_out != nullptr;
-    const int blocks = k3_blocks(c, c->search == 1, wc);
+    const int blocks = k3_blocks(c, wc);
     TRY(loop_buffers(c, blocks, 1));
     init_state(c, T_in, 0, 0.0, 0.0, 1);
     CK(cudaMemcpyAsync(c->state.p, c->h_state, sizeof(IcpState), cudaMemcpyHostToDevice, c->exec));
@@ -618,7 +631,7 @@ o3g_status o3g_icp_run(o3g_ctx* c, const double init_T[16], int32_t max_iteratio
     if (!c->src_ready) return fail(O3G_ERR_INVALID_ARGUMENT, "o3g_set_target and o3g_set_source must be called first");
     if (!T_out || !fitness || !inlier_rmse) return fail(O3G_ERR_INVALID_ARGUMENT, "T_out, fitness and inlier_rmse are required");
     TRY(enter(c));
-    const int blocks = k3_blocks(c, c->search == 1, false);
+    const int blocks = k3_blocks(c, false);
     TRY(loop_buffers(c, blocks, max_iterations + 1));
     init_state(c, init_T, max_iterations, relative_fitness, relative_rmse, max_iterations + 1);
     CK(cudaMemcpyAsync(c->state.p, c->h_state, sizeof(IcpState), cudaMemcpyHostToDevice, c->exec));

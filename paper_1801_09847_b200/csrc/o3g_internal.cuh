@@ -60,10 +60,11 @@ __host__ __device__ inline uint32_t grid_row_hash(int cy, int cz) {
 // fp64 without contraction; clamped to [-2, n+1] so far queries cannot
 // overflow (they have no candidates anyway). Used identically for the
 // target points (grid build) and the transformed queries (search).
+// (cvt.rmi.s32.f64 floors and saturates out-of-range values, then the int
+// clamp; identical to clamping in fp64 first for every finite x.)
 __device__ __forceinline__ int cell_coord(double x, double o, double inv_h, int n) {
-    double c = floor(__dmul_rn(__dsub_rn(x, o), inv_h));
-    c = fmin(fmax(c, -2.0), (double)n + 1.0);
-    return (int)c;
+    const int c = __double2int_rd(__dmul_rn(__dsub_rn(x, o), inv_h));
+    return min(max(c, -2), n + 1);
 }
 
 // A3: s' = T s, fixed order ((T00 sx + T01 sy) + T02 sz) + T03, no FMA (R2).
@@ -90,6 +91,12 @@ void launch_gather_target(const float* xyz, const float* nrm, const int32_t* val
 void launch_gather_source(const float* xyz, const int32_t* vals_sorted, int64_t lo, int64_t hi,
                           float4* out, cudaStream_t s);
 void launch_fill_i32(int32_t* p, int64_t n, int32_t v, cudaStream_t s);
+// dilated occupancy bitmap of a dense grid: occupancy from cell_start, then
+// three shifted-OR passes (x by 1, y by nx, z by nx*ny). Bits that wrap across
+// row / slab boundaries only add false positives (a query then just does the
+// full search). Result in `out` (words = ceil(ncells / 32)).
+void launch_nbr_bits(const int32_t* cell_start, int64_t ncells, int64_t nx, int64_t nxny,
+                     uint32_t* tmp, uint32_t* out, cudaStream_t s);
 
 // ---- launchers (icp_kernels.cu)
 struct K3Args {
@@ -104,9 +111,17 @@ struct K3Args {
     const IcpState* st;
     double* block_partials; // [gridDim.x][kTermStride]
     int32_t* corr_out;      // original order, nullable
+    const uint32_t* nbr_bits;  // dense grid: bit k set iff some cell of k's 27-stencil
+                               // is occupied (a conservative skip test); nullable
 };
-void launch_k3(const K3Args& a, int blocks, bool prefilter, bool write_corr, cudaStream_t s);
-int k3_max_blocks_per_sm(bool prefilter, bool write_corr);
+// variant: 0 = exact fp64 scan (k3_corr_reduce), 1 = two-pass warp kernel
+// (k3_balanced), 2 = single-pass prefilter (k3_corr_reduce<true>), 3 = tile-sorted
+// two-pass kernel (k3_sorted, default). Identical correspondences.
+inline int k3_threads(int variant) { return variant == 3 ? 128 : kK3Threads; }
+int k3_sorted_blocks_per_sm(bool write_corr, int hashed);
+void launch_k3_sorted(const K3Args& a, int blocks, bool write_corr, cudaStream_t s);
+void launch_k3(const K3Args& a, int blocks, int variant, bool write_corr, cudaStream_t s);
+int k3_max_blocks_per_sm(int variant, bool write_corr, int hashed);
 void launch_tail(const double* block_partials, int nblocks, double* gathered, int world, int rank,
                  IcpState* st, double* hist_fit, double* hist_rmse, int mode, cudaStream_t s);
 

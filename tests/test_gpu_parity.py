@@ -19,7 +19,7 @@ pytestmark = pytest.mark.gpu
 torch = pytest.importorskip("torch")
 GOLD = os.path.join(os.path.dirname(__file__), "golden")
 
-SEARCH = {"exact": 0, "prefilter": 1}
+SEARCH = {"exact": 0, "balanced": 1, "prefilter": 2, "sorted": 3}
 GRID = {"dense": 1, "hashed": 2}
 
 
@@ -36,7 +36,7 @@ def _dev(a):
     return torch.from_numpy(np.ascontiguousarray(a, np.float32)).cuda()
 
 
-def _ctx(o3g, w, search="prefilter", grid="dense", order_T=None, src=None):
+def _ctx(o3g, w, search="balanced", grid="dense", order_T=None, src=None):
     ctx = o3g.Context(0)
     ctx.set_option(1, SEARCH[search])
     ctx.set_option(2, GRID[grid])
@@ -173,7 +173,7 @@ def test_hashed_grid_matches_dense(o3g, workloads):
     T = w["T_true"] @ _perturb(4, 0.01, 0.01)
     out = {}
     for grid in GRID:
-        with _ctx(o3g, w, "prefilter", grid) as ctx:
+        with _ctx(o3g, w, "balanced", grid) as ctx:
             out[grid] = _step(ctx, T, len(w["source"]))
             info = ctx.grid_info()
             assert info["hashed"] == (grid == "hashed")
@@ -207,7 +207,7 @@ def test_loop_parity_lidar_subsample(o3g, workloads):
     sub = np.sort(Stream(13).integers(3000, len(w["source"])))
     src = w["source"][sub]
     ref = oracle.icp(src, w["target"], w["target_normals"], w["dmax"], 10)
-    with _ctx(o3g, w, "prefilter", src=src) as ctx:
+    with _ctx(o3g, w, "balanced", src=src) as ctx:
         r = ctx.run(np.eye(4), 10)
     assert np.abs(r.transformation - ref["T"]).max() <= 1e-6
     assert abs(r.fitness - ref["fitness"]) <= 1e-6 and abs(r.inlier_rmse - ref["inlier_rmse"]) <= 1e-6
@@ -350,3 +350,15 @@ def test_large16m_full_size_sampled(o3g, workloads):
     # 3 deg about the scene centre moves far points ~1.3 m >> dmax: the loop
     # only partially recovers (SURVEY §8(d) caveat), but fitness must improve
     assert r.hist_fitness[-1] > r.hist_fitness[0]
+
+
+def test_neighbour_mask_off_matches(o3g, workloads):
+    """The dilated-occupancy skip (O3G_OPT_NBR_MASK) never changes results."""
+    w = workloads("large16m", n=400_000)
+    out = []
+    for mask in (1, 0):
+        with _ctx(o3g, w, "balanced") as ctx:
+            ctx.set_option(5, mask)
+            out.append(_step(ctx, w["T_true"], len(w["source"])))
+    assert np.array_equal(out[0][0], out[1][0])
+    assert np.array_equal(out[0][1]["terms"], out[1][1]["terms"])

@@ -166,6 +166,9 @@ __host__ __device__ inline size_t k3v2_warp_bytes(int hashed) {
 }
 inline size_t k3v2_smem(int hashed) { return (size_t)(kK3Threads / 32) * k3v2_warp_bytes(hashed); }
 
+__device__ __noinline__ void tail_finish(const double* terms, IcpState* st, double* hist_fit, double* hist_rmse,
+                            int mode);
+
 template <bool WRITE_CORR>
 __global__ void __launch_bounds__(kK3Threads, 4) k3_balanced(const K3Args a) {
     extern __shared__ __align__(16) unsigned char k3smem[];
@@ -187,8 +190,52 @@ __global__ void __launch_bounds__(kK3Threads, 4) k3_balanced(const K3Args a) {
     const int nw = gridDim.x * (kK3Threads / 32);
     const int* __restrict__ cs = a.cell_start;
     const int nxny = g.nx * g.ny;
-    for (int base = gw * 32; base < a.n; base += nw * 32) {
-        const int i = base + lane;
+    // Live-query queue (dense grid with the occupancy bitmap): a first cheap
+    // pass per batch of 32 (s' = T s, cell, one bitmap bit) drops queries
+    // whose 27-cell stencil is empty; the rest are queued per warp and the
+    // full search runs on full warps of live queries only.
+    __shared__ int qbuf[kK3Threads / 32][64];
+    const bool use_queue = a.nbr_bits != nullptr;
+    int qn = 0;   // warp-uniform queue length
+    int base = gw * 32;
+    for (;;) {
+        int i;
+        if (use_queue) {
+        while (qn < 32 && base < a.n) {
+            const int i0 = base + lane;
+            base += nw * 32;
+            bool live = false;
+            if (i0 < a.n) {
+                const float4 p0 = __ldg(&a.src[i0]);
+                double tx, ty, tz;
+                xform_rn(sT, p0.x, p0.y, p0.z, tx, ty, tz);
+                const int cx = cell_coord(tx, g.ox, g.inv_h, g.nx);
+                const int cy = cell_coord(ty, g.oy, g.inv_h, g.ny);
+                const int cz = cell_coord(tz, g.oz, g.inv_h, g.nz);
+                if (cx >= -1 && cx <= g.nx && cy >= -1 && cy <= g.ny && cz >= -1 && cz <= g.nz) {
+                    const int kc = (min(max(cz, 0), g.nz - 1) * g.ny + min(max(cy, 0), g.ny - 1)) * g.nx +
+                                   min(max(cx, 0), g.nx - 1);
+                    live = (__ldg(&a.nbr_bits[kc >> 5]) >> (kc & 31)) & 1u;
+                }
+                if (WRITE_CORR && !live) a.corr_out[__float_as_int(p0.w)] = -1;
+            }
+            const unsigned lb = __ballot_sync(0xffffffffu, live);
+            if (live) qbuf[warp][qn + __popc(lb & ((1u << lane) - 1u))] = i0;
+            qn += __popc(lb);
+            __syncwarp();
+        }
+        if (qn == 0) break;
+        const int take = min(qn, 32);
+        i = lane < take ? qbuf[warp][lane] : a.n;
+        __syncwarp();
+        if (lane + 32 < qn) qbuf[warp][lane] = qbuf[warp][lane + 32];
+        __syncwarp();
+        qn -= take;
+        } else {
+            if (base >= a.n) break;
+            i = base + lane;
+            base += nw * 32;
+        }
         double sx = 0.0, sy = 0.0, sz = 0.0, E1 = 0.0;
         float shx = 0.f, shy = 0.f, shz = 0.f, thr0 = 0.f;
         int nseg = 0, c = 0;
@@ -371,6 +418,31 @@ __global__ void __launch_bounds__(kK3Threads, 4) k3_balanced(const K3Args a) {
         }
         a.block_partials[(size_t)blockIdx.x * kTermStride + threadIdx.x] = s;
     }
+    if (!a.fuse_mode) return;
+
+    // fused A6 grid step + A8: the last block reduces every block partial in
+    // the same fixed order as k_tail (lane-strided, then butterfly) and
+    // finishes the pass; it resets the counter for the next launch.
+    __shared__ unsigned int s_last;
+    __shared__ double terms[kTermStride];
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = atomicAdd(a.counter, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    for (int t = warp; t < kTerms; t += kK3Threads / 32) {
+        double s = 0.0;
+        for (int b = lane; b < (int)gridDim.x; b += 32) s += __ldcg(&a.block_partials[(size_t)b * kTermStride + t]);
+#pragma unroll
+        for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane == 0) terms[t] = s;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        *a.counter = 0u;
+        tail_finish(terms, a.st_rw, a.hist_fit, a.hist_rmse, a.fuse_mode);
+    }
 }
 
 template <bool P, bool W>
@@ -484,36 +556,10 @@ __device__ static void se3_exp(const double* xi, double* E /*3x4*/) {
     }
 }
 
-__global__ void __launch_bounds__(kTailThreads)
-    k_tail(const double* __restrict__ partials, int nblocks, double* gathered, int world, int rank,
-           IcpState* st, double* hist_fit, double* hist_rmse, int mode) {
-    __shared__ double terms[kTermStride];
-    if (!(mode & TAIL_STEP) && st->done) return;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (mode & TAIL_REDUCE_BLOCKS) {
-        if (warp < kTerms) {
-            double s = 0.0;
-            for (int b = lane; b < nblocks; b += 32) s += partials[(size_t)b * kTermStride + warp];
-#pragma unroll
-            for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-            if (lane == 0) terms[warp] = s;
-        }
-        __syncthreads();
-        if (mode & TAIL_WRITE_RANK) {
-            if (threadIdx.x < kTermStride)
-                gathered[rank * kTermStride + threadIdx.x] = threadIdx.x < kTerms ? terms[threadIdx.x] : 0.0;
-            return;
-        }
-    }
-    if (mode & TAIL_SUM_RANKS) {
-        if (threadIdx.x < kTerms) {
-            double s = 0.0;
-            for (int r = 0; r < world; ++r) s += gathered[r * kTermStride + threadIdx.x];
-            terms[threadIdx.x] = s;
-        }
-        __syncthreads();
-    }
-    if (threadIdx.x != 0) return;
+// Thread-0 epilogue of a pass (A8): store the 29 terms; in SOLVE mode apply the
+// criteria (R7, R8) and the Gauss-Newton update (Eq. 2, R5, R6) to the state.
+__device__ __noinline__ void tail_finish(const double* terms, IcpState* st, double* hist_fit, double* hist_rmse,
+                            int mode) {
     for (int k = 0; k < kTerms; ++k) st->terms[k] = terms[k];
     if (mode & TAIL_STEP) return;
 
@@ -567,6 +613,39 @@ __global__ void __launch_bounds__(kTailThreads)
     }
     if (done && cnt == 0.0) st->flags |= 1;  // O3G_FLAG_NO_CORRESPONDENCES
     st->done = done;
+}
+
+__global__ void __launch_bounds__(kTailThreads)
+    k_tail(const double* __restrict__ partials, int nblocks, double* gathered, int world, int rank,
+           IcpState* st, double* hist_fit, double* hist_rmse, int mode) {
+    __shared__ double terms[kTermStride];
+    if (!(mode & TAIL_STEP) && st->done) return;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (mode & TAIL_REDUCE_BLOCKS) {
+        if (warp < kTerms) {
+            double s = 0.0;
+            for (int b = lane; b < nblocks; b += 32) s += partials[(size_t)b * kTermStride + warp];
+#pragma unroll
+            for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+            if (lane == 0) terms[warp] = s;
+        }
+        __syncthreads();
+        if (mode & TAIL_WRITE_RANK) {
+            if (threadIdx.x < kTermStride)
+                gathered[rank * kTermStride + threadIdx.x] = threadIdx.x < kTerms ? terms[threadIdx.x] : 0.0;
+            return;
+        }
+    }
+    if (mode & TAIL_SUM_RANKS) {
+        if (threadIdx.x < kTerms) {
+            double s = 0.0;
+            for (int r = 0; r < world; ++r) s += gathered[r * kTermStride + threadIdx.x];
+            terms[threadIdx.x] = s;
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x != 0) return;
+    tail_finish(terms, st, hist_fit, hist_rmse, mode);
 }
 
 void launch_tail(const double* partials, int nblocks, double* gathered, int world, int rank,

@@ -336,6 +336,7 @@ o3g_status o3g_set_target(o3g_ctx* c, const float* xyz, const float* normals, in
     unsigned long long* occ = (unsigned long long*)(mm + 8);
     CK(cudaMemsetAsync(mm, 0xFF, 12, c->exec));
     CK(cudaMemsetAsync(mm + 3, 0x00, 12 + 4 + 4 + 8, c->exec));
+    CK(cudaMemsetAsync(mm + 12, 0x00, 4, c->exec));   // fused-tail block counter
     launch_bbox(dx, n, mm, bad, c->sms, c->exec);
     launch_check_finite(dn, 3 * n, bad, c->sms, c->exec);
     c->launches += 2;
@@ -492,6 +493,10 @@ static K3Args k3_args(o3g_ctx* c, int32_t* corr) {
     a.block_partials = c->partials.as<double>();
     a.corr_out = corr;
     a.nbr_bits = (c->nbr_mask && c->nbr_ready) ? c->nbr_a.as<uint32_t>() : nullptr;
+    a.fuse_mode = 0;
+    a.counter = nullptr;
+    a.st_rw = nullptr;
+    a.hist_fit = a.hist_rmse = nullptr;
     return a;
 }
 
@@ -499,15 +504,26 @@ static K3Args k3_args(o3g_ctx* c, int32_t* corr) {
 static o3g_status enqueue_pass(o3g_ctx* c, int blocks, bool write_corr, int32_t* corr,
                                int tail_mode, cudaEvent_t ev0, cudaEvent_t ev1, int* nlaunch) {
     if (ev0) CK(cudaEventRecordWithFlags(ev0, c->exec, cudaEventRecordExternal));
+    const bool fused = c->world == 1 && c->search == 1 && c->n_local > 0;
     if (c->n_local > 0) {
-        launch_k3(k3_args(c, corr), blocks, c->search, write_corr, c->exec);
+        K3Args ka = k3_args(c, corr);
+        if (fused) {
+            ka.fuse_mode = tail_mode;
+            ka.counter = c->misc.as<unsigned int>() + 12;   // see set_target's misc layout
+            ka.st_rw = c->state.as<IcpState>();
+            ka.hist_fit = c->hist_fit.as<double>();
+            ka.hist_rmse = c->hist_rmse.as<double>();
+        }
+        launch_k3(ka, blocks, c->search, write_corr, c->exec);
         ++*nlaunch;
     }
     if (ev1) CK(cudaEventRecordWithFlags(ev1, c->exec, cudaEventRecordExternal));
     const int nb = c->n_local > 0 ? blocks : 0;
     double* gat = c->gathered.as<double>();
     IcpState* st = c->state.as<IcpState>();
-    if (c->world == 1) {
+    if (fused) {
+        // A6/A8 ran in the last K3 block
+    } else if (c->world == 1) {
         launch_tail(c->partials.as<double>(), nb, gat, 1, 0, st, c->hist_fit.as<double>(),
                     c->hist_rmse.as<double>(), TAIL_REDUCE_BLOCKS | tail_mode, c->exec);
         ++*nlaunch;

@@ -113,6 +113,13 @@ struct K3Args {
     int32_t* corr_out;      // original order, nullable
     const uint32_t* nbr_bits;  // dense grid: bit k set iff some cell of k's 27-stencil
                                // is occupied (a conservative skip test); nullable
+    // fused tail (single GPU, variant 1): the last block to finish reduces the
+    // block partials in fixed order and runs the A8 epilogue (mode = TAIL_*)
+    int fuse_mode;             // 0 = separate k_tail launch
+    unsigned int* counter;     // zero between launches (the last block resets it)
+    IcpState* st_rw;
+    double* hist_fit;
+    double* hist_rmse;
 };
 // variant: 0 = exact fp64 scan (k3_corr_reduce), 1 = two-pass warp kernel
 // (k3_balanced), 2 = single-pass prefilter (k3_corr_reduce<true>), 3 = tile-sorted

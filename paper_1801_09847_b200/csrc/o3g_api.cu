@@ -380,7 +380,7 @@ o3g_status o3g_set_target(o3g_ctx* c, const float* xyz, const float* normals, in
     TRY(c->vals_b.ensure(n * 4));
     TRY(c->cell_start.ensure((g.table_size + 1) * 4));
     TRY(c->counts.ensure((g.table_size + 1) * 4));
-    TRY(c->tpos.ensure(n * sizeof(float4)));
+    TRY(c->tpos.ensure((n + 2) * sizeof(float4)));   // +pad: pair loads may touch tpos[n]
     TRY(c->tnrm.ensure(n * sizeof(float4)));
 
     launch_cell_keys(dx, n, g, nullptr, c->keys_a.as<uint32_t>(), c->vals_a.as<int32_t>(), c->exec);

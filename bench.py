@@ -45,6 +45,7 @@ def parse():
     ap.add_argument("--config", default="large16m")
     ap.add_argument("--iters", type=int, default=None)
     ap.add_argument("--search", type=int, default=1, help="K3 variant: 0 exact fp64 scan, 1 two-pass warp (default), 2 single-pass prefilter, 3 tile-sorted two-pass")
+    ap.add_argument("--coop-min", type=int, default=None, help="override O3G_OPT_COOP_MIN")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--n", type=int, default=None, help="override point count (testing only)")
@@ -52,12 +53,17 @@ def parse():
 
 
 def load_workload(name, n=None):
+    """The named BASELINE config. `fragment` carries per-scale parameters and
+    its step runs the whole multi-scale driver (downsampling included)."""
     from synth import make
     kw = {"n": n} if (n is not None and name in ("large16m", "fragment", "tiny")) else {}
-    w = make(name, **kw)
-    if name == "fragment":      # finest scale is the timed registration
-        w = w["scales"][-1]
-    return w
+    return make(name, **kw)
+
+
+def oracle_view(w):
+    """The single registration the CPU oracle samples (finest scale of a
+    multi-scale config)."""
+    return w["scales"][-1] if "scales" in w else w
 
 
 def peaks():
@@ -148,7 +154,7 @@ def run_reference(a):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    w = load_workload(a.config, a.n)
+    w = oracle_view(load_workload(a.config, a.n))
     import oracle
     oracle.build()
     budget = max(2.0, 150.0 / max(1, a.steps + a.warmup))
@@ -195,15 +201,29 @@ def main():
 
     ctx = o3g.Context(local)
     ctx.set_option(o3g.o3g.OPT_SEARCH, a.search)
+    if a.coop_min is not None:
+        ctx.set_option(6, a.coop_min)
     if world > 1:
         uid = [o3g.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
         ctx.dist_init(rank, world, uid[0])
 
+    multiscale = "scales" in w
+    if multiscale:
+        vox = [sc["meta"]["voxel"] for sc in w["scales"]]
+        dms = [sc["dmax"] for sc in w["scales"]]
+        its = [sc["iters"] if a.iters is None else a.iters for sc in w["scales"]]
+
     def step(s_, t_, n_):
+        """One full registration; returns the source-point-iterations it did."""
+        if multiscale:
+            r = ctx.run_multiscale(s_, t_, n_, vox, dms, its, init=T0, relative_fitness=0.0,
+                                   relative_rmse=0.0)
+            return int(np.sum(r["n_source"] * r["iterations"])), r
         ctx.set_target(t_, n_, w["dmax"])
         ctx.set_source(s_, T0)
-        return ctx.run(T0, iters, 0.0, 0.0)
+        r = ctx.run(T0, iters, 0.0, 0.0)
+        return n * r.iterations, r
 
     def barrier():
         torch.cuda.synchronize()
@@ -211,52 +231,79 @@ def main():
             dist.barrier()
 
     for _ in range(a.warmup):
-        res = step(src, tgt, nrm)
+        units, res = step(src, tgt, nrm)
     barrier()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     l0 = ctx.launch_count()
+    # inputs smaller than the 126 MB L2 are flushed (a 256 MB write) before
+    # every timed step and only the steps themselves are timed
+    in_bytes = 12 * n + 24 * m
+    flush = in_bytes < 126 * 2 ** 20
+    scratch = torch.empty(256 * 2 ** 20, dtype=torch.uint8, device=dev) if flush else None
     with Clocks(local) as clk:
-        ev0.record()
-        for _ in range(a.steps):
-            res = step(src, tgt, nrm)
-        ev1.record()
-        barrier()
+        if not flush:
+            ev0.record()
+            for _ in range(a.steps):
+                units, res = step(src, tgt, nrm)
+            ev1.record()
+            barrier()
+            ms = ev0.elapsed_time(ev1) / a.steps
+        else:
+            tot = 0.0
+            for _ in range(a.steps):
+                scratch.fill_(1)
+                ev0.record()
+                units, res = step(src, tgt, nrm)
+                ev1.record()
+                torch.cuda.synchronize()
+                tot += ev0.elapsed_time(ev1)
+            barrier()
+            ms = tot / a.steps
     launches = (ctx.launch_count() - l0) // a.steps * a.steps
-    ms = ev0.elapsed_time(ev1) / a.steps
     if world > 1:
         t = torch.tensor([ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    updates = res.iterations
-    value = n * updates / (ms / 1e3)
+    value = units / (ms / 1e3)
 
     # dominant kernel (K3) live duration with CUDA events inside the run graph
     ctx.set_option(o3g.o3g.OPT_TIMING, 1)
-    ctx.set_target(tgt, nrm, w["dmax"])
-    ctx.set_source(src, T0)
     t_loop = []
     k3 = []
     for _ in range(3):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        r2 = ctx.run(T0, iters, 0.0, 0.0)
-        e1.record()
+        if multiscale:       # K3 of the finest scale (the last run of the driver)
+            e0.record()
+            units2, r2 = step(src, tgt, nrm)
+            e1.record()
+        else:
+            ctx.set_target(tgt, nrm, w["dmax"])
+            ctx.set_source(src, T0)
+            e0.record()
+            r2 = ctx.run(T0, iters, 0.0, 0.0)
+            e1.record()
+            units2 = n * r2.iterations
         torch.cuda.synchronize()
-        t_loop.append(e0.elapsed_time(e1))
+        t_loop.append((e0.elapsed_time(e1), units2))
         k3_ms, k3_n, tail_ms = ctx.last_run_kernel_ms()
         k3.append((k3_ms, k3_n, tail_ms))
     ctx.set_option(o3g.o3g.OPT_TIMING, 0)
     k3_ms, k3_n, tail_ms = min(k3)
     k3_avg = k3_ms / k3_n
     hbm, peak_kind = peaks()
-    n_local = (rank + 1) * n // world - rank * n // world
-    alg_bytes = 12 * n_local + 24 * m / world
+    if multiscale:
+        n_k3 = int(r2["n_source"][-1])
+        m_k3 = len(w["scales"][-1]["target"])
+    else:
+        n_k3, m_k3 = n, m
+    n_local = (rank + 1) * n_k3 // world - rank * n_k3 // world
+    alg_bytes = 12 * n_local + 24 * m_k3 / world
     achieved = alg_bytes / (k3_avg / 1e3) / 1e9
     traffic = None
     tp = os.path.join(ROOT, "profiles", "k3_traffic.json")
     if os.path.exists(tp):
         traffic = json.load(open(tp)).get(f"{a.config}@{world}")
-    loop_ms = min(t_loop)
+    loop_ms, loop_units = min(t_loop)
 
     # e2e: same metric through the C ABI one-shot call with pinned HOST buffers
     e2e = None
@@ -266,11 +313,10 @@ def main():
         hn = torch.from_numpy(w["target_normals"]).pin_memory()
 
         def e2e_step():
-            if world == 1:
+            if world == 1 and not multiscale:
                 r = o3g.icp_point_to_plane(hs, ht, hn, w["dmax"], T0, iters, 0.0, 0.0)
-            else:
-                r = step(hs, ht, hn)
-            return r
+                return n * r.iterations
+            return step(hs, ht, hn)[0]
         e2e_step()
         barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -284,7 +330,7 @@ def main():
             t = torch.tensor([ems], device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ems = float(t.item())
-        e2e = {"value": n * r3.iterations / (ems / 1e3), "unit": UNIT, "ms_per_step": ems,
+        e2e = {"value": r3 / (ems / 1e3), "unit": UNIT, "ms_per_step": ems,
                "h2d_bytes_per_step": 12 * n + 24 * m,
                "d2h_bytes_per_step": 472 + 32 + 8 + 4}
 
@@ -292,7 +338,7 @@ def main():
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
         import oracle
         oracle.build()
-        cpu = cpu_oracle_rate(w)
+        cpu = cpu_oracle_rate(oracle_view(w))
 
     if rank == 0:
         out = {
@@ -300,11 +346,14 @@ def main():
             "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": a.config, "n_source": n, "n_target": m, "dmax": w["dmax"],
-                       "iterations": iters, "updates_per_step": updates,
+                       "iterations": iters, "src_pt_iterations_per_step": units,
+                       "scales": ([{"voxel": v, "dmax": d, "iters": k} for v, d, k in zip(vox, dms, its)]
+                                  if multiscale else None),
                        "parallelism": f"source-shard x{world}, target grid replicated",
                        "search": ["exact-fp64", "two-pass fp32-prefilter+exact-fp64", "single-pass fp32-prefilter+exact-fp64", "tile-sorted two-pass fp32-prefilter+exact-fp64"][a.search],
-                       "l2": "inputs 576 MB > 126 MB L2 (no flush needed)" if a.config == "large16m"
-                             else "inputs resident; L2-resident working set"},
+                       "l2": (f"inputs {in_bytes / 1e6:.0f} MB < 126 MB L2: 256 MB write flushes L2 before "
+                              "each timed step" if flush else
+                              f"inputs {in_bytes / 1e6:.0f} MB > 126 MB L2 (no flush needed)")},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "traffic": traffic, "peak_kind": peak_kind,
                          "kernel": "k3_corr_reduce", "kernel_ms": k3_avg,
@@ -313,9 +362,10 @@ def main():
             "e2e": e2e,
             "gpu_launches": launches,
             "clocks": clk.summary(),
-            "detail": {"loop_ms": loop_ms, "loop_src_pt_it_per_s": n * r2.iterations / (loop_ms / 1e3),
+            "detail": {"loop_ms": loop_ms, "loop_src_pt_it_per_s": loop_units / (loop_ms / 1e3),
                        "k3_total_ms": k3_ms, "tail_total_ms": tail_ms, "k3_launches": k3_n,
-                       "fitness": res.fitness, "inlier_rmse": res.inlier_rmse,
+                       "fitness": (float(res["fitness"][-1]) if multiscale else res.fitness),
+                       "inlier_rmse": (float(res["inlier_rmse"][-1]) if multiscale else res.inlier_rmse),
                        "grid": ctx.grid_info()},
         }
         print(json.dumps(out), flush=True)

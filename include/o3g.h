@@ -137,6 +137,35 @@ o3g_status o3g_icp_run(o3g_ctx* ctx, const double init_T[16], int32_t max_iterat
                        double* fitness, double* inlier_rmse, o3g_icp_info* info,
                        double* hist_fitness, double* hist_rmse);
 
+/* ------------------------------------------- downsampling and multi-scale
+ * voxel_down_sample (Fig. 1): each output point
+ * is the mean of the input points of one occupied voxel of the grid anchored
+ * at the cloud's minimum bound, index floor((p - min) / voxel) per axis;
+ * normals (nullable) are averaged the same way and renormalised (a zero sum
+ * stays zero); output in ascending lexicographic (ix, iy, iz) order.
+ * Sums are fp64 in original-index order, the mean is rounded once to fp32.
+ * xyz / normals: [n][3] float32, host or device. out_xyz / out_normals:
+ * DEVICE float32 [n][3] capacity (out_normals may be NULL). *n_out: host.
+ * O3G_ERR_INVALID_ARGUMENT for n <= 0, voxel <= 0 or non-finite input, or
+ * more than 2^63 voxels in the bounding box.                            */
+o3g_status o3g_voxel_down_sample(o3g_ctx* ctx, const float* xyz, const float* normals, int64_t n,
+                                 double voxel, float* out_xyz, float* out_normals, int64_t* n_out);
+
+/* Multi-scale point-to-plane ICP (BASELINE config 4):
+ * for s = 0..n_scales-1, downsample source and target (with normals) at
+ * voxel[s], run the loop of o3g_icp_run with max_correspondence_distance
+ * dmax[s] and max_iterations iters[s] starting from the current T, and
+ * carry T to the next scale (R13). Arrays of length n_scales are
+ * host memory; the per-scale outputs (nullable) receive fitness, inlier
+ * rmse, updates applied and the downsampled source size of each scale.   */
+o3g_status o3g_icp_multiscale(o3g_ctx* ctx, const float* source_xyz, int64_t n_source,
+                              const float* target_xyz, const float* target_normals,
+                              int64_t n_target, const double init_T[16], int32_t n_scales,
+                              const double* voxel, const double* dmax, const int32_t* iters,
+                              double relative_fitness, double relative_rmse, double T_out[16],
+                              double* fitness_per_scale, double* rmse_per_scale,
+                              int32_t* iterations_per_scale, int64_t* n_source_per_scale);
+
 /* ------------------------------------------------------------ multi-GPU
  * One process per GPU. Rank 0 calls o3g_nccl_unique_id (128 bytes), the
  * caller broadcasts it (e.g. torch.distributed), every rank calls
@@ -159,10 +188,13 @@ o3g_status o3g_dist_init(o3g_ctx* ctx, int rank, int world, const void* nccl_uni
  *   kernel inside the run graph (read with o3g_last_run_kernel_ms).
  * O3G_OPT_BLOCKS_PER_SM: override the persistent grid size (0 = auto).
  * O3G_OPT_NBR_MASK: 1 = skip queries whose 27-cell stencil is empty using a
- *   dilated occupancy bitmap of the dense grid (default), 0 = off. Results
- *   are identical either way.                                            */
+ *   dilated occupancy bitmap of the dense grid (default), 0 = off.
+ * O3G_OPT_COOP_MIN: variant 1 scans a query with at least this many
+ *   candidates with the whole warp (0 = never; -1 = auto, the default:
+ *   256 when the target averages >= 32 points per occupied cell, else 0).
+ * Results are identical for every option value.                         */
 enum { O3G_OPT_SEARCH = 1, O3G_OPT_GRID = 2, O3G_OPT_TIMING = 3, O3G_OPT_BLOCKS_PER_SM = 4,
-       O3G_OPT_NBR_MASK = 5 };
+       O3G_OPT_NBR_MASK = 5, O3G_OPT_COOP_MIN = 6 };
 o3g_status o3g_set_option(o3g_ctx* ctx, int option, int64_t value);
 
 /* Sum of the correspondence-kernel (K3) durations of the last o3g_icp_run

@@ -57,12 +57,18 @@ def lib():
         L.orc_compose.argtypes = [P, P, P]
         L.orc_icp.restype = C.c_int
         L.orc_icp.argtypes = [P, I64, P, P, I64, P, D, I32, D, D, I32, P, P, P, P, P, P, P, P]
+        L.orc_voxel_down_sample.restype = I64
+        L.orc_voxel_down_sample.argtypes = [P, P, I64, D, P, P]
+        L.orc_icp_multiscale.restype = C.c_int
+        L.orc_icp_multiscale.argtypes = [P, I64, P, P, I64, P, I32, P, P, P, D, D, P, P, P, P, P]
         _lib = L
     return _lib
 
 
 def _p(a):
-    return a.ctypes.data if a is not None else None
+    # the ctypes view keeps the array alive for the duration of the call
+    # (a bare .ctypes.data of a temporary copy would dangle)
+    return a.ctypes if a is not None else None
 
 
 def _f32(a):
@@ -170,3 +176,35 @@ def icp(source, target, normals, dmax, max_iterations, init_T=None, relative_fit
     return dict(T=T.reshape(4, 4), fitness=float(fit[0]), inlier_rmse=float(rmse[0]),
                 iterations=int(it[0]), flags=int(fl[0]), converged=bool(cv[0]), passes=passes,
                 hist_fitness=hf[:passes].copy(), hist_rmse=hr[:passes].copy())
+
+
+def voxel_down_sample(points, voxel, normals=None):
+    """SPEC S:58-61 voxel_down_sample (see o3g_oracle.c). Returns (points,
+    normals or None) as float32 arrays in ascending (ix, iy, iz) order."""
+    p = _f32(points)
+    nr = None if normals is None else _f32(normals)
+    out_p = np.empty_like(p)
+    out_n = None if nr is None else np.empty_like(nr)
+    k = lib().orc_voxel_down_sample(_p(p), _p(nr), len(p), float(voxel), _p(out_p), _p(out_n))
+    if k < 0:
+        raise ValueError("voxel_down_sample: invalid input")
+    return out_p[:k].copy(), (None if out_n is None else out_n[:k].copy())
+
+
+def icp_multiscale(source, target, normals, voxels, dmaxs, iters, init_T=None,
+                   relative_fitness=1e-6, relative_rmse=1e-6):
+    """Multi-scale point-to-plane ICP (downsample per scale, carry T)."""
+    src, tgt, nrm = _f32(source), _f32(target), _f32(normals)
+    ns = len(voxels)
+    T0 = _f64(np.eye(4) if init_T is None else init_T)
+    T = np.zeros(16)
+    fit, rmse = np.zeros(ns), np.zeros(ns)
+    its = np.zeros(ns, np.int32)
+    nss = np.zeros(ns, np.int64)
+    rc = lib().orc_icp_multiscale(_p(src), len(src), _p(tgt), _p(nrm), len(tgt), _p(T0), ns,
+                                  _p(_f64(voxels)), _p(_f64(dmaxs)),
+                                  _p(np.ascontiguousarray(iters, np.int32)), float(relative_fitness),
+                                  float(relative_rmse), _p(T), _p(fit), _p(rmse), _p(its), _p(nss))
+    if rc != 0:
+        raise RuntimeError("oracle multiscale failed")
+    return dict(T=T.reshape(4, 4), fitness=fit, inlier_rmse=rmse, iterations=its, n_source=nss)

@@ -408,3 +408,100 @@ int orc_icp(const float *src, int64_t n, const float *tgt, const float *nrm, int
     orc_grid_free(g);
     return passes;
 }
+
+/* ------------------------------------------------- voxel_down_sample (NEXT 1) */
+/* SPEC S:58-61 (Fig. 1 "voxel_size = 0.05"): each output point is the
+ * arithmetic mean of the input points in one occupied voxel of the grid
+ * anchored at the cloud's minimum bound, voxel index floor((p - min)/voxel)
+ * (floor semantics); normals averaged the same way then renormalised;
+ * output in ascending lexicographic (ix, iy, iz) order. Sums are fp64 in
+ * original index order; mean = sum / count rounded once to fp32; normal =
+ * s / sqrt((sx*sx + sy*sy) + sz*sz) (zero if the sum is zero). Returns the
+ * number of output points.                                               */
+typedef struct { int64_t ix, iy, iz, idx; } orc_vox;
+
+static int cmp_vox(const void *a_, const void *b_)
+{
+    const orc_vox *a = (const orc_vox *)a_, *b = (const orc_vox *)b_;
+    if (a->ix != b->ix) return a->ix < b->ix ? -1 : 1;
+    if (a->iy != b->iy) return a->iy < b->iy ? -1 : 1;
+    if (a->iz != b->iz) return a->iz < b->iz ? -1 : 1;
+    return a->idx < b->idx ? -1 : (a->idx > b->idx);
+}
+
+int64_t orc_voxel_down_sample(const float *p, const float *nrm, int64_t n, double voxel,
+                              float *out_p, float *out_n)
+{
+    if (n <= 0 || !(voxel > 0.0)) return -1;
+    double mn[3] = {INFINITY, INFINITY, INFINITY};
+    for (int64_t i = 0; i < n; ++i)
+        for (int a = 0; a < 3; ++a)
+            if ((double)p[3 * i + a] < mn[a]) mn[a] = (double)p[3 * i + a];
+    orc_vox *v = (orc_vox *)malloc(sizeof(orc_vox) * (size_t)n);
+    if (!v) return -2;
+    for (int64_t i = 0; i < n; ++i) {
+        v[i].ix = (int64_t)floor(((double)p[3 * i + 0] - mn[0]) / voxel);
+        v[i].iy = (int64_t)floor(((double)p[3 * i + 1] - mn[1]) / voxel);
+        v[i].iz = (int64_t)floor(((double)p[3 * i + 2] - mn[2]) / voxel);
+        v[i].idx = i;
+    }
+    qsort(v, (size_t)n, sizeof(orc_vox), cmp_vox);
+    int64_t out = 0;
+    for (int64_t s = 0; s < n;) {
+        int64_t e = s;
+        double sp[3] = {0, 0, 0}, sn[3] = {0, 0, 0};
+        while (e < n && v[e].ix == v[s].ix && v[e].iy == v[s].iy && v[e].iz == v[s].iz) {
+            for (int a = 0; a < 3; ++a) {
+                sp[a] += (double)p[3 * v[e].idx + a];
+                if (nrm) sn[a] += (double)nrm[3 * v[e].idx + a];
+            }
+            ++e;
+        }
+        const double cnt = (double)(e - s);
+        for (int a = 0; a < 3; ++a) out_p[3 * out + a] = (float)(sp[a] / cnt);
+        if (nrm && out_n) {
+            double nn = sqrt((sn[0] * sn[0] + sn[1] * sn[1]) + sn[2] * sn[2]);
+            for (int a = 0; a < 3; ++a) out_n[3 * out + a] = nn > 0.0 ? (float)(sn[a] / nn) : 0.0f;
+        }
+        ++out;
+        s = e;
+    }
+    free(v);
+    return out;
+}
+
+/* Multi-scale registration (NEXT 1; SURVEY §8(c) reading R13): for each
+ * scale s, downsample source and target at voxel[s] (target normals
+ * averaged), run orc_icp with dmax[s] and iters[s] from the current T, and
+ * carry T to the next scale. fit/rmse/iterations of each scale are written
+ * to the per-scale arrays (nullable).                                      */
+int orc_icp_multiscale(const float *src, int64_t n, const float *tgt, const float *nrm, int64_t m,
+                       const double T0[16], int32_t nscales, const double *voxel, const double *dmax,
+                       const int32_t *iters, double relative_fitness, double relative_rmse,
+                       double T_out[16], double *fit_s, double *rmse_s, int32_t *iters_s,
+                       int64_t *nsrc_s)
+{
+    double T[16];
+    memcpy(T, T0, sizeof(T));
+    float *sp = (float *)malloc(sizeof(float) * 3 * (size_t)n);
+    float *tp = (float *)malloc(sizeof(float) * 3 * (size_t)m);
+    float *tn = (float *)malloc(sizeof(float) * 3 * (size_t)m);
+    if (!sp || !tp || !tn) { free(sp); free(tp); free(tn); return -1; }
+    for (int32_t s = 0; s < nscales; ++s) {
+        int64_t ns = orc_voxel_down_sample(src, NULL, n, voxel[s], sp, NULL);
+        int64_t ms = orc_voxel_down_sample(tgt, nrm, m, voxel[s], tp, tn);
+        double fit, rmse, Tn[16];
+        int32_t it, fl, cv;
+        if (ns <= 0 || ms <= 0) { free(sp); free(tp); free(tn); return -1; }
+        orc_icp(sp, ns, tp, tn, ms, T, dmax[s], iters[s], relative_fitness, relative_rmse, 1, Tn,
+                &fit, &rmse, &it, &fl, &cv, NULL, NULL);
+        memcpy(T, Tn, sizeof(T));
+        if (fit_s) fit_s[s] = fit;
+        if (rmse_s) rmse_s[s] = rmse;
+        if (iters_s) iters_s[s] = it;
+        if (nsrc_s) nsrc_s[s] = ns;
+    }
+    memcpy(T_out, T, sizeof(T));
+    free(sp); free(tp); free(tn);
+    return 0;
+}

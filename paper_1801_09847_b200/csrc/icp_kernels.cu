@@ -169,7 +169,7 @@ inline size_t k3v2_smem(int hashed) { return (size_t)(kK3Threads / 32) * k3v2_wa
 __device__ __noinline__ void tail_finish(const double* terms, IcpState* st, double* hist_fit, double* hist_rmse,
                             int mode);
 
-template <bool WRITE_CORR>
+template <bool WRITE_CORR, bool COOP>
 __global__ void __launch_bounds__(kK3Threads, 4) k3_balanced(const K3Args a) {
     extern __shared__ __align__(16) unsigned char k3smem[];
     __shared__ double sT[12];
@@ -313,14 +313,102 @@ __global__ void __launch_bounds__(kK3Threads, 4) k3_balanced(const K3Args a) {
             }
         }
 
-        // pass 1: branch-free fp32 scan of every candidate of this lane's query
+        int win = -1, widx = -1;
+        double wd2 = 0.0;
+        float4 wq = make_float4(0.f, 0.f, 0.f, 0.f);
+
+        // heavy queries (>= coop_min candidates, e.g. LiDAR near the sensor): the
+        // whole warp scans one query at a time with coalesced lane-strided loads,
+        // merges (m1, j1, m2) by butterfly, and decides cooperatively (the same
+        // exact rule; ties and near-ties take a cooperative exact rescan).
+        const bool heavy = COOP && c >= a.coop_min;
+        unsigned hv = COOP ? __ballot_sync(0xffffffffu, heavy) : 0u;
+        while (COOP && hv) {
+            const int q = __ffs(hv) - 1;
+            hv &= hv - 1u;
+            const float qx = __shfl_sync(0xffffffffu, shx, q), qy = __shfl_sync(0xffffffffu, shy, q),
+                        qz = __shfl_sync(0xffffffffu, shz, q), qthr0 = __shfl_sync(0xffffffffu, thr0, q);
+            const int qseg = __shfl_sync(0xffffffffu, nseg, q);
+            float lm1 = CUDART_INF_F, lm2 = CUDART_INF_F;
+            int lj1 = INT_MAX;
+            for (int k = 0; k < qseg; ++k) {
+                const int2 sg = segs[k * 32 + q];
+#pragma unroll 4
+                for (int j = sg.x + lane; j < sg.y; j += 32) {
+                    const float4 t = __ldg(&a.tpos[j]);
+                    const float ux = t.x - qx, uy = t.y - qy, uz = t.z - qz;
+                    const float df = fmaf(uz, uz, fmaf(uy, uy, ux * ux));
+                    const bool lt = df < lm1;
+                    lm2 = fminf(lm2, lt ? lm1 : df);
+                    lm1 = lt ? df : lm1;
+                    lj1 = lt ? j : lj1;
+                }
+            }
+#pragma unroll
+            for (int o = 16; o; o >>= 1) {   // (m1, j1) lexicographic min; m2 = 2nd smallest
+                const float om1 = __shfl_xor_sync(0xffffffffu, lm1, o);
+                const float om2 = __shfl_xor_sync(0xffffffffu, lm2, o);
+                const int oj1 = __shfl_xor_sync(0xffffffffu, lj1, o);
+                lm2 = fminf(fminf(lm2, om2), fmaxf(lm1, om1));
+                const bool take = om1 < lm1 || (om1 == lm1 && oj1 < lj1);
+                lj1 = take ? oj1 : lj1;
+                lm1 = fminf(lm1, om1);
+            }
+            const double qsx = __shfl_sync(0xffffffffu, sx, q), qsy = __shfl_sync(0xffffffffu, sy, q),
+                         qsz = __shfl_sync(0xffffffffu, sz, q), qE1 = __shfl_sync(0xffffffffu, E1, q);
+            int cw = -1, cidx = -1;
+            double cd2 = 0.0;
+            float4 cq = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (lm1 <= qthr0) {
+                const float4 t = __ldg(&a.tpos[lj1]);
+                const double dx = __dsub_rn(qsx, (double)t.x), dy = __dsub_rn(qsy, (double)t.y),
+                             dz = __dsub_rn(qsz, (double)t.z);
+                const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+                const double B = d2 <= r2 ? d2 : r2;
+                const float thB = prefilter_thr(B, qE1, a.dmax, a.inv_dmax);
+                if (lm2 > thB) {
+                    if (d2 <= r2) cw = lj1, cidx = __float_as_int(t.w), cd2 = d2, cq = t;
+                } else {
+                    // cooperative exact rescan: the winner has d2 <= B, so df <= thr(B)
+                    double bd = CUDART_INF;
+                    int bidx = INT_MAX, bj = -1;
+                    for (int k = 0; k < qseg; ++k) {
+                        const int2 sg = segs[k * 32 + q];
+                        for (int j = sg.x + lane; j < sg.y; j += 32) {
+                            const float4 u = __ldg(&a.tpos[j]);
+                            const float ux = u.x - qx, uy = u.y - qy, uz = u.z - qz;
+                            if (fmaf(uz, uz, fmaf(uy, uy, ux * ux)) > thB) continue;
+                            const double ex = __dsub_rn(qsx, (double)u.x), ey = __dsub_rn(qsy, (double)u.y),
+                                         ez = __dsub_rn(qsz, (double)u.z);
+                            const double e2 = __dadd_rn(__dadd_rn(__dmul_rn(ex, ex), __dmul_rn(ey, ey)),
+                                                        __dmul_rn(ez, ez));
+                            const int idx = __float_as_int(u.w);
+                            if (e2 <= r2 && (e2 < bd || (e2 == bd && idx < bidx))) bd = e2, bidx = idx, bj = j;
+                        }
+                    }
+#pragma unroll
+                    for (int o = 16; o; o >>= 1) {
+                        const double od = __shfl_xor_sync(0xffffffffu, bd, o);
+                        const int oi = __shfl_xor_sync(0xffffffffu, bidx, o);
+                        const int oj = __shfl_xor_sync(0xffffffffu, bj, o);
+                        const bool take = od < bd || (od == bd && oi < bidx);
+                        bd = take ? od : bd, bidx = take ? oi : bidx, bj = take ? oj : bj;
+                    }
+                    if (bj >= 0) cw = bj, cidx = bidx, cd2 = bd, cq = __ldg(&a.tpos[bj]);
+                }
+            }
+            if (lane == q) win = cw, widx = cidx, wd2 = cd2, wq = cq;
+        }
+
+        // pass 1 (light queries): branch-free fp32 scan of every candidate of this lane's query
         float m1 = CUDART_INF_F, m2 = CUDART_INF_F;
         int j1 = -1;
+        const int cl = heavy ? 0 : c;
         {
             int k = 0;
-            int2 sg = c > 0 ? segs[lane] : make_int2(0, 0);
+            int2 sg = cl > 0 ? segs[lane] : make_int2(0, 0);
             int j = sg.x, e = sg.y;
-            for (int it = 0; it < c; ++it) {
+            for (int it = 0; it < cl; ++it) {
                 if (j == e) {
                     ++k;
                     sg = segs[k * 32 + lane];
@@ -338,10 +426,7 @@ __global__ void __launch_bounds__(kK3Threads, 4) k3_balanced(const K3Args a) {
         }
 
         // decision (exact fp64 rule, R1-R3)
-        int win = -1, widx = -1;
-        double wd2 = 0.0;
-        float4 wq = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (c > 0 && m1 <= thr0) {
+        if (cl > 0 && m1 <= thr0) {
             const float4 t = __ldg(&a.tpos[j1]);
             const double dx = __dsub_rn(sx, (double)t.x), dy = __dsub_rn(sy, (double)t.y),
                          dz = __dsub_rn(sz, (double)t.z);
@@ -452,16 +537,16 @@ static int occ_of() {
     return b;
 }
 
-template <bool W>
+template <bool W, bool CO>
 static int occ_v2(int hashed) {
-    static bool attr_done[2] = {false, false};
-    if (!attr_done[hashed]) {
-        cudaFuncSetAttribute(k3_balanced<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    static bool attr_done = false;
+    if (!attr_done) {
+        cudaFuncSetAttribute(k3_balanced<W, CO>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)k3v2_smem(1));
-        attr_done[hashed] = true;
+        attr_done = true;
     }
     int b = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k3_balanced<W>, kK3Threads, k3v2_smem(hashed));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k3_balanced<W, CO>, kK3Threads, k3v2_smem(hashed));
     return b;
 }
 
@@ -470,7 +555,8 @@ int k3_max_blocks_per_sm(int variant, bool write_corr, int hashed) {
         case 0: return write_corr ? occ_of<false, true>() : occ_of<false, false>();
         case 2: return write_corr ? occ_of<true, true>() : occ_of<true, false>();
         case 3: return k3_sorted_blocks_per_sm(write_corr, hashed);
-        default: return write_corr ? occ_v2<true>(hashed) : occ_v2<false>(hashed);
+        default:   // the cooperative instantiation has the same footprint class
+            return write_corr ? occ_v2<true, false>(hashed) : occ_v2<false, false>(hashed);
     }
 }
 
@@ -487,10 +573,15 @@ void launch_k3(const K3Args& a, int blocks, int variant, bool write_corr, cudaSt
         case 3: launch_k3_sorted(a, blocks, write_corr, s); break;
         default: {
             const size_t sm = k3v2_smem(a.g.hashed);
-            occ_v2<true>(a.g.hashed);
-            occ_v2<false>(a.g.hashed);
-            if (write_corr) k3_balanced<true><<<blocks, kK3Threads, sm, s>>>(a);
-            else k3_balanced<false><<<blocks, kK3Threads, sm, s>>>(a);
+            occ_v2<true, false>(a.g.hashed), occ_v2<false, false>(a.g.hashed);
+            occ_v2<true, true>(a.g.hashed), occ_v2<false, true>(a.g.hashed);
+            if (a.coop_min > 0) {
+                if (write_corr) k3_balanced<true, true><<<blocks, kK3Threads, sm, s>>>(a);
+                else k3_balanced<false, true><<<blocks, kK3Threads, sm, s>>>(a);
+            } else {
+                if (write_corr) k3_balanced<true, false><<<blocks, kK3Threads, sm, s>>>(a);
+                else k3_balanced<false, false><<<blocks, kK3Threads, sm, s>>>(a);
+            }
         }
     }
 }

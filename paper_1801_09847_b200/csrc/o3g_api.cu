@@ -119,7 +119,7 @@ struct o3g_ctx {
     cudaEvent_t fence = nullptr;
 
     // options
-    int search = 1, grid_mode = 0, timing = 0, bps_override = 0, nbr_mask = 1;
+    int search = 1, grid_mode = 0, timing = 0, bps_override = 0, nbr_mask = 1, coop_min = -1;
 
     // target grid
     int64_t m = 0;
@@ -130,6 +130,8 @@ struct o3g_ctx {
     bool nbr_ready = false;
     // scratch
     DevBuf keys_a, keys_b, vals_a, vals_b, cub_tmp, stage_a, stage_b, misc;
+    // voxel_down_sample / multi-scale scratch
+    DevBuf vk_a, vk_b, vflags, vrunid, vstarts, ms_src, ms_tgt, ms_nrm;
     // source
     int64_t n_total = 0, n_local = 0, shard_lo = 0;
     bool src_ready = false;
@@ -282,7 +284,9 @@ o3g_status o3g_destroy(o3g_ctx* c) {
     for (auto ev : c->events) cudaEventDestroy(ev);
     DevBuf* bufs[] = {&c->tpos, &c->tnrm, &c->cell_start, &c->counts, &c->nbr_a, &c->nbr_b, &c->keys_a, &c->keys_b,
                       &c->vals_a, &c->vals_b, &c->cub_tmp, &c->stage_a, &c->stage_b, &c->misc,
-                      &c->src4, &c->partials, &c->gathered, &c->state, &c->hist_fit, &c->hist_rmse};
+                      &c->src4, &c->partials, &c->gathered, &c->state, &c->hist_fit, &c->hist_rmse,
+                      &c->vk_a, &c->vk_b, &c->vflags, &c->vrunid, &c->vstarts, &c->ms_src,
+                      &c->ms_tgt, &c->ms_nrm};
     for (DevBuf* b : bufs) b->release();
     if (c->comm && nccl().comm_destroy) nccl().comm_destroy(c->comm);
     if (c->h_state) cudaFreeHost(c->h_state);
@@ -305,6 +309,10 @@ o3g_status o3g_set_option(o3g_ctx* c, int option, int64_t value) {
             break;
         case O3G_OPT_TIMING: c->timing = value ? 1 : 0; break;
         case O3G_OPT_NBR_MASK: c->nbr_mask = value ? 1 : 0; break;
+        case O3G_OPT_COOP_MIN:
+            if (value < -1 || value > (1 << 30)) return fail(O3G_ERR_INVALID_ARGUMENT, "coop_min out of range");
+            c->coop_min = (int)value;
+            break;
         case O3G_OPT_BLOCKS_PER_SM:
             if (value < 0 || value > 64) return fail(O3G_ERR_INVALID_ARGUMENT, "blocks per SM out of range");
             c->bps_override = (int)value;
@@ -493,6 +501,10 @@ static K3Args k3_args(o3g_ctx* c, int32_t* corr) {
     a.block_partials = c->partials.as<double>();
     a.corr_out = corr;
     a.nbr_bits = (c->nbr_mask && c->nbr_ready) ? c->nbr_a.as<uint32_t>() : nullptr;
+    // auto (-1): warp-cooperative scans only where cells are dense (measured:
+    // LiDAR, 226 points per occupied cell, gains 1.6x; sparse configs lose)
+    a.coop_min = c->coop_min >= 0 ? c->coop_min
+                                  : ((double)c->m >= 32.0 * (double)(c->occupied > 0 ? c->occupied : 1) ? 256 : 0);
     a.fuse_mode = 0;
     a.counter = nullptr;
     a.st_rw = nullptr;
@@ -747,6 +759,120 @@ o3g_status o3g_dist_init(o3g_ctx* c, int rank, int world, const void* id) {
         return fail(O3G_ERR_COMM, std::string("ncclCommInitRank: ") +
                                       (nccl().error_string ? nccl().error_string(r) : "?"));
     }
+    return O3G_OK;
+}
+
+// ------------------------------------------------- voxel downsample
+static o3g_status voxel_impl(o3g_ctx* c, const float* xyz, const float* normals, int64_t n,
+                             double voxel, float* out_xyz, float* out_nrm, int64_t* n_out) {
+    if (n <= 0 || n > 0x7ffffffeLL) return fail(O3G_ERR_INVALID_ARGUMENT, "n must be in [1, 2^31-2]");
+    if (!(voxel > 0.0) || !isfinite(voxel)) return fail(O3G_ERR_INVALID_ARGUMENT, "voxel must be finite and > 0");
+    if (!xyz || !out_xyz || !n_out) return fail(O3G_ERR_INVALID_ARGUMENT, "xyz, out_xyz and n_out are required");
+    TRY(enter(c));
+    const float *dx, *dn = nullptr;
+    TRY(device_view(c, xyz, 3 * n, c->stage_a, &dx));
+    if (normals) TRY(device_view(c, normals, 3 * n, c->stage_b, &dn));
+    TRY(c->misc.ensure(64));
+    uint32_t* mm = c->misc.as<uint32_t>();
+    int32_t* bad = (int32_t*)(mm + 6);
+    CK(cudaMemsetAsync(mm, 0xFF, 12, c->exec));
+    CK(cudaMemsetAsync(mm + 3, 0x00, 12 + 4, c->exec));
+    launch_bbox(dx, n, mm, bad, c->sms, c->exec);
+    if (dn) launch_check_finite(dn, 3 * n, bad, c->sms, c->exec);
+    c->launches += dn ? 2 : 1;
+    uint32_t h[7];
+    CK(cudaMemcpyAsync(h, mm, 28, cudaMemcpyDeviceToHost, c->exec));
+    CK(cudaStreamSynchronize(c->exec));
+    if (h[6]) return fail(O3G_ERR_INVALID_ARGUMENT, "non-finite coordinate or normal");
+    double mn[3];
+    double cells = 1.0;
+    uint64_t dims[3];
+    for (int a = 0; a < 3; ++a) {
+        mn[a] = (double)ord2f(h[a]);
+        const double d = floor(((double)ord2f(h[3 + a]) - mn[a]) / voxel) + 1.0;
+        dims[a] = (uint64_t)d;
+        cells *= d;
+    }
+    if (!(cells < 9.0e18)) return fail(O3G_ERR_INVALID_ARGUMENT, "too many voxels in the bounding box");
+    TRY(c->vk_a.ensure(n * 8));
+    TRY(c->vk_b.ensure(n * 8));
+    TRY(c->vals_a.ensure(n * 4));
+    TRY(c->vals_b.ensure(n * 4));
+    TRY(c->vflags.ensure(n * 4));
+    TRY(c->vrunid.ensure(n * 4));
+    TRY(c->vstarts.ensure((n + 1) * 4));
+    launch_vox_keys(dx, n, mn, voxel, dims[1], dims[2], c->vk_a.as<uint64_t>(), c->vals_a.as<int32_t>(), c->exec);
+    int bits = 1;
+    while (bits < 64 && ((uint64_t)(cells - 1.0) >> bits)) ++bits;
+    size_t tmp = 0;
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp, c->vk_a.as<uint64_t>(), c->vk_b.as<uint64_t>(),
+                                       c->vals_a.as<int32_t>(), c->vals_b.as<int32_t>(), (int)n, 0, bits, c->exec));
+    TRY(c->cub_tmp.ensure(tmp));
+    CK(cub::DeviceRadixSort::SortPairs(c->cub_tmp.p, tmp, c->vk_a.as<uint64_t>(), c->vk_b.as<uint64_t>(),
+                                       c->vals_a.as<int32_t>(), c->vals_b.as<int32_t>(), (int)n, 0, bits, c->exec));
+    launch_run_flags(c->vk_b.as<uint64_t>(), n, c->vflags.as<int32_t>(), c->exec);
+    tmp = 0;
+    CK(cub::DeviceScan::InclusiveSum(nullptr, tmp, c->vflags.as<int32_t>(), c->vrunid.as<int32_t>(), (int)n, c->exec));
+    TRY(c->cub_tmp.ensure(tmp));
+    CK(cub::DeviceScan::InclusiveSum(c->cub_tmp.p, tmp, c->vflags.as<int32_t>(), c->vrunid.as<int32_t>(), (int)n, c->exec));
+    launch_run_starts(c->vflags.as<int32_t>(), c->vrunid.as<int32_t>(), n, c->vstarts.as<int32_t>(), c->exec);
+    int32_t nruns = 0;
+    CK(cudaMemcpyAsync(&nruns, c->vrunid.as<int32_t>() + (n - 1), 4, cudaMemcpyDeviceToHost, c->exec));
+    CK(cudaStreamSynchronize(c->exec));
+    launch_vox_mean(dx, dn, c->vals_b.as<int32_t>(), c->vstarts.as<int32_t>(), nruns, out_xyz,
+                    dn ? out_nrm : nullptr, c->exec);
+    c->launches += 4;
+    CK(cudaStreamSynchronize(c->exec));
+    CK(cudaGetLastError());
+    *n_out = nruns;
+    return O3G_OK;
+}
+
+extern "C" o3g_status o3g_voxel_down_sample(o3g_ctx* c, const float* xyz, const float* normals, int64_t n,
+                                            double voxel, float* out_xyz, float* out_normals,
+                                            int64_t* n_out) {
+    if (!c) return fail(O3G_ERR_INVALID_ARGUMENT, "ctx is NULL");
+    if (out_xyz && !is_device_ptr(out_xyz)) return fail(O3G_ERR_INVALID_ARGUMENT, "out_xyz must be device memory");
+    if (out_normals && !is_device_ptr(out_normals)) return fail(O3G_ERR_INVALID_ARGUMENT, "out_normals must be device memory");
+    return voxel_impl(c, xyz, normals, n, voxel, out_xyz, out_normals, n_out);
+}
+
+extern "C" o3g_status o3g_icp_multiscale(o3g_ctx* c, const float* src, int64_t n, const float* tgt,
+                                         const float* nrm, int64_t m, const double init_T[16],
+                                         int32_t ns, const double* voxel, const double* dmax,
+                                         const int32_t* iters, double rel_fit, double rel_rmse,
+                                         double T_out[16], double* fit_s, double* rmse_s,
+                                         int32_t* it_s, int64_t* n_s) {
+    if (!c) return fail(O3G_ERR_INVALID_ARGUMENT, "ctx is NULL");
+    if (ns <= 0 || !voxel || !dmax || !iters) return fail(O3G_ERR_INVALID_ARGUMENT, "need n_scales > 0 and per-scale arrays");
+    if (!init_T || !rigid_ok(init_T)) return fail(O3G_ERR_INVALID_ARGUMENT, "init_T is not a rigid transform");
+    if (!T_out) return fail(O3G_ERR_INVALID_ARGUMENT, "T_out is required");
+    if (!src || !tgt || !nrm) return fail(O3G_ERR_INVALID_ARGUMENT, "source, target and normals are required");
+    for (int s = 0; s < ns; ++s)
+        if (iters[s] < 0 || !(dmax[s] > 0.0) || !(voxel[s] > 0.0))
+            return fail(O3G_ERR_INVALID_ARGUMENT, "invalid per-scale parameters");
+    if (n <= 0 || m <= 0) return fail(O3G_ERR_INVALID_ARGUMENT, "empty cloud");
+    TRY(c->ms_src.ensure((size_t)n * 12));
+    TRY(c->ms_tgt.ensure((size_t)m * 12));
+    TRY(c->ms_nrm.ensure((size_t)m * 12));
+    double T[16];
+    memcpy(T, init_T, sizeof(T));
+    for (int s = 0; s < ns; ++s) {
+        int64_t nsrc = 0, ntgt = 0;
+        TRY(voxel_impl(c, tgt, nrm, m, voxel[s], c->ms_tgt.as<float>(), c->ms_nrm.as<float>(), &ntgt));
+        TRY(o3g_set_target(c, c->ms_tgt.as<float>(), c->ms_nrm.as<float>(), ntgt, dmax[s]));
+        TRY(voxel_impl(c, src, nullptr, n, voxel[s], c->ms_src.as<float>(), nullptr, &nsrc));
+        TRY(o3g_set_source(c, c->ms_src.as<float>(), nsrc, T));
+        double fit = 0, rmse = 0, Tn[16];
+        o3g_icp_info info;
+        TRY(o3g_icp_run(c, T, iters[s], rel_fit, rel_rmse, Tn, &fit, &rmse, &info, nullptr, nullptr));
+        memcpy(T, Tn, sizeof(T));
+        if (fit_s) fit_s[s] = fit;
+        if (rmse_s) rmse_s[s] = rmse;
+        if (it_s) it_s[s] = info.iterations;
+        if (n_s) n_s[s] = nsrc;
+    }
+    memcpy(T_out, T, sizeof(T));
     return O3G_OK;
 }
 

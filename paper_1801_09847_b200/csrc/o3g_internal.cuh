@@ -98,6 +98,15 @@ void launch_fill_i32(int32_t* p, int64_t n, int32_t v, cudaStream_t s);
 void launch_nbr_bits(const int32_t* cell_start, int64_t ncells, int64_t nx, int64_t nxny,
                      uint32_t* tmp, uint32_t* out, cudaStream_t s);
 
+// ---- launchers (voxel.cu)
+void launch_vox_keys(const float* xyz, int64_t n, const double mn[3], double voxel, uint64_t dy,
+                     uint64_t dz, uint64_t* keys, int32_t* vals, cudaStream_t s);
+void launch_run_flags(const uint64_t* keys, int64_t n, int32_t* flags, cudaStream_t s);
+void launch_run_starts(const int32_t* flags, const int32_t* runid, int64_t n, int32_t* starts,
+                       cudaStream_t s);
+void launch_vox_mean(const float* xyz, const float* nrm, const int32_t* vals, const int32_t* starts,
+                     int64_t nruns, float* out_xyz, float* out_nrm, cudaStream_t s);
+
 // ---- launchers (icp_kernels.cu)
 struct K3Args {
     const float4* src;      // sorted local shard (x,y,z, bitcast original index)
@@ -113,6 +122,8 @@ struct K3Args {
     int32_t* corr_out;      // original order, nullable
     const uint32_t* nbr_bits;  // dense grid: bit k set iff some cell of k's 27-stencil
                                // is occupied (a conservative skip test); nullable
+    int coop_min;              // variant 1: queries with >= coop_min candidates are
+                               // scanned by the whole warp (0 = never)
     // fused tail (single GPU, variant 1): the last block to finish reduces the
     // block partials in fixed order and runs the A8 epilogue (mode = TAIL_*)
     int fuse_mode;             // 0 = separate k_tail launch

@@ -68,6 +68,8 @@ def lib() -> C.CDLL:
             "o3g_set_option": [P, C.c_int, I64],
             "o3g_last_run_kernel_ms": [P, P, P, P],
             "o3g_grid_info": [P, P, P, P, P],
+            "o3g_voxel_down_sample": [P, P, P, I64, D, P, P, P],
+            "o3g_icp_multiscale": [P, P, I64, P, P, I64, P, I32, P, P, P, D, D, P, P, P, P, P],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -257,6 +259,45 @@ class Context:
         if history:
             hf, hr = hf[:info.passes].copy(), hr[:info.passes].copy()
         return _result(T, fit, rmse, info, hf, hr)
+
+    def voxel_down_sample(self, xyz, voxel, normals=None):
+        """SPEC S:58-61 voxel_down_sample on the device. Returns CUDA tensors
+        (points [k,3], normals [k,3] or None)."""
+        import torch
+        keep: list = []
+        p, n = _pts(xyz, "xyz", keep)
+        pn, nn = _pts(normals, "normals", keep)
+        if pn is not None and nn != n:
+            raise InvalidArgument(ERR_INVALID_ARGUMENT, "normals must match xyz")
+        dev = torch.device("cuda", self.device)
+        out = torch.empty((max(n, 1), 3), dtype=torch.float32, device=dev)
+        outn = torch.empty((max(n, 1), 3), dtype=torch.float32, device=dev) if pn is not None else None
+        k = C.c_int64()
+        _check(lib().o3g_voxel_down_sample(self._h, p, pn, n, float(voxel), out.data_ptr(),
+                                           outn.data_ptr() if outn is not None else None, C.byref(k)))
+        return out[:k.value], (outn[:k.value] if outn is not None else None)
+
+    def run_multiscale(self, source, target, target_normals, voxels, dmaxs, iters, init=None,
+                       relative_fitness=1e-6, relative_rmse=1e-6) -> dict:
+        """Multi-scale point-to-plane ICP (o3g_icp_multiscale)."""
+        keep: list = []
+        ps, n = _pts(source, "source", keep)
+        pt, m = _pts(target, "target", keep)
+        pn, _ = _pts(target_normals, "target_normals", keep)
+        ns = len(voxels)
+        vx = np.ascontiguousarray(voxels, np.float64)
+        dm = np.ascontiguousarray(dmaxs, np.float64)
+        it = np.ascontiguousarray(iters, np.int32)
+        T = np.zeros(16)
+        fit, rmse = np.zeros(ns), np.zeros(ns)
+        its, nss = np.zeros(ns, np.int32), np.zeros(ns, np.int64)
+        _check(lib().o3g_icp_multiscale(self._h, ps, n, pt, pn, m,
+                                        _mat(np.eye(4) if init is None else init, keep), ns,
+                                        vx.ctypes.data, dm.ctypes.data, it.ctypes.data,
+                                        float(relative_fitness), float(relative_rmse), T.ctypes.data,
+                                        fit.ctypes.data, rmse.ctypes.data, its.ctypes.data,
+                                        nss.ctypes.data))
+        return dict(T=T.reshape(4, 4), fitness=fit, inlier_rmse=rmse, iterations=its, n_source=nss)
 
     def last_run_kernel_ms(self):
         k3, n, tail = C.c_double(), C.c_int32(), C.c_double()

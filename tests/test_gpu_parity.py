@@ -363,3 +363,25 @@ def test_neighbour_mask_off_matches(o3g, workloads):
             out.append(_step(ctx, w["T_true"], len(w["source"])))
     assert np.array_equal(out[0][0], out[1][0])
     assert np.array_equal(out[0][1]["terms"], out[1][1]["terms"])
+
+
+@pytest.mark.parametrize("name", ["depth", "lidar"])
+def test_cooperative_threshold_invariance(o3g, workloads, name):
+    """O3G_OPT_COOP_MIN (warp-cooperative scan of heavy queries) never changes
+    the correspondences: all queries cooperative (1), default (64), none (0)."""
+    w = workloads(name)
+    T = w["T_true"] @ _perturb(21, 0.004, 0.01)
+    sub = None if name == "depth" else Stream(22).integers(3000, len(w["source"]))
+    ref = oracle.step(T, w["source"], w["target"], w["target_normals"], w["dmax"],
+                      grid=oracle.Grid(w["target"], w["dmax"]), subset=sub)
+    outs = []
+    for cm in (1, 64, 0):
+        with _ctx(o3g, w, "balanced") as ctx:
+            ctx.set_option(6, cm)
+            corr, st = _step(ctx, T, len(w["source"]))
+        got = corr if sub is None else corr[sub]
+        assert np.array_equal(got, ref["corr"]), cm
+        outs.append((corr, st))
+        if sub is None:
+            _terms_ok(st["terms"], ref)
+    assert np.array_equal(outs[0][0], outs[2][0])

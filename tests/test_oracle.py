@@ -327,3 +327,60 @@ def test_convergence_criteria_semantics(workloads):
     assert abs(hf[k] - hf[k - 1]) < 1e-6 and abs(hr[k] - hr[k - 1]) < 1e-6
     for i in range(1, k):
         assert not (abs(hf[i] - hf[i - 1]) < 1e-6 and abs(hr[i] - hr[i - 1]) < 1e-6)
+
+
+# ------------------------------------------------ voxel_down_sample (NEXT 1)
+def test_voxel_down_sample_spec_examples():
+    """singleton -> same point; two points in one voxel -> their mean."""
+    p, _ = oracle.voxel_down_sample(np.array([[0.01, 0.01, 0.01]], np.float32), 0.05)
+    assert np.array_equal(p, np.array([[0.01, 0.01, 0.01]], np.float32))
+    p, _ = oracle.voxel_down_sample(np.array([[0, 0, 0], [0.01, 0, 0]], np.float32), 0.05)
+    assert np.array_equal(p, np.array([[0.005, 0, 0]], np.float32))
+
+
+def test_voxel_down_sample_matches_bucketing():
+    """equals an independent bucketing oracle (numpy unique + bincount,
+    a different summation order: compare within 1 fp32 ulp) and keeps the
+    S:124-126 invariants (count <= n, each mean inside its voxel, ascending
+    lexicographic voxel order, unit normals)."""
+    rs = Stream(77)
+    p = rs.uniform(30000, -1, 1).reshape(-1, 3).astype(np.float32)
+    nr = rs.unit_vectors(len(p)).astype(np.float32)
+    voxel = 0.05
+    out, outn = oracle.voxel_down_sample(p, voxel, nr)
+    p64 = p.astype(np.float64)
+    lo = p64.min(0)
+    ijk = np.floor((p64 - lo) / voxel).astype(np.int64)
+    key = (ijk[:, 0] * 10000 + ijk[:, 1]) * 10000 + ijk[:, 2]
+    uniq, inv, cnt = np.unique(key, return_inverse=True, return_counts=True)
+    ref = np.stack([np.bincount(inv, p64[:, a]) for a in range(3)], 1) / cnt[:, None]
+    assert len(out) == len(uniq) <= len(p)
+    assert np.all(np.abs(out - ref.astype(np.float32)) <= np.spacing(np.abs(ref).astype(np.float32)) * 1.01)
+    vox_of_out = np.floor((out.astype(np.float64) - lo) / voxel).astype(np.int64)
+    assert np.array_equal((vox_of_out[:, 0] * 10000 + vox_of_out[:, 1]) * 10000 + vox_of_out[:, 2], uniq)
+    norms = np.linalg.norm(outn.astype(np.float64), axis=1)
+    assert np.all(np.abs(norms - 1) < 1e-6) or np.all((np.abs(norms - 1) < 1e-6) | (norms == 0))
+
+
+def test_multiscale_single_scale_is_downsample_then_icp():
+    """One scale of the multi-scale driver == voxel_down_sample + icp."""
+    rs = Stream(31338)
+    tgt, nrm = _scene_small(rs, 6000)
+    tgt = tgt.astype(np.float32)
+    M = rigid(rotation([0.2, 0.5, 1.0], math.radians(1.0)), [0.01, -0.01, 0.005])
+    src = apply(M, tgt.astype(np.float64)).astype(np.float32)
+    ms = oracle.icp_multiscale(src, tgt, nrm, [0.03], [0.1], [20])
+    sd, _ = oracle.voxel_down_sample(src, 0.03)
+    td, tn = oracle.voxel_down_sample(tgt, 0.03, nrm)
+    r = oracle.icp(sd, td, tn, 0.1, 20)
+    assert np.array_equal(ms["T"], r["T"]) and ms["fitness"][0] == r["fitness"]
+
+
+def test_multiscale_recovers_motion():
+    rs = Stream(31339)
+    tgt, nrm = _scene_small(rs, 20000)
+    tgt = tgt.astype(np.float32)
+    M = rigid(rotation([0.2, 0.5, 1.0], math.radians(2.0)), [0.03, -0.02, 0.01])
+    src = apply(M, tgt.astype(np.float64)).astype(np.float32)
+    ms = oracle.icp_multiscale(src, tgt, nrm, [0.08, 0.04, 0.02], [0.16, 0.08, 0.04], [30, 20, 10])
+    assert np.abs(ms["T"] - inv_rigid(M)).max() < 2e-3

@@ -15,6 +15,7 @@ ap.add_argument("--iters", type=int, default=None)
 ap.add_argument("--mode", default="run", choices=["run", "step"])
 ap.add_argument("--search", type=int, default=1)
 ap.add_argument("--bps", type=int, default=0)
+ap.add_argument("--coop-min", type=int, default=None)
 a = ap.parse_args()
 
 import torch  # noqa: E402
@@ -29,6 +30,8 @@ ctx = o3g.Context(0)
 ctx.set_option(1, a.search)
 if a.bps:
     ctx.set_option(4, a.bps)
+if a.coop_min is not None:
+    ctx.set_option(6, a.coop_min)
 for _ in range(a.reps):
     ctx.set_target(tgt, nrm, w["dmax"])
     ctx.set_source(src, w["init_T"])

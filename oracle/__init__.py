@@ -59,6 +59,11 @@ def lib():
         L.orc_icp.argtypes = [P, I64, P, P, I64, P, D, I32, D, D, I32, P, P, P, P, P, P, P, P]
         L.orc_voxel_down_sample.restype = I64
         L.orc_voxel_down_sample.argtypes = [P, P, I64, D, P, P]
+        L.orc_pass_p2p.argtypes = [P, P, I64, P, I64, P, D, P, P]
+        L.orc_kabsch.restype = C.c_int
+        L.orc_kabsch.argtypes = [P, P]
+        L.orc_icp_p2p.restype = C.c_int
+        L.orc_icp_p2p.argtypes = [P, I64, P, I64, P, D, I32, D, D, P, P, P, P, P, P]
         L.orc_icp_multiscale.restype = C.c_int
         L.orc_icp_multiscale.argtypes = [P, I64, P, P, I64, P, I32, P, P, P, D, D, P, P, P, P, P]
         _lib = L
@@ -208,3 +213,38 @@ def icp_multiscale(source, target, normals, voxels, dmaxs, iters, init_T=None,
     if rc != 0:
         raise RuntimeError("oracle multiscale failed")
     return dict(T=T.reshape(4, 4), fitness=fit, inlier_rmse=rmse, iterations=its, n_source=nss)
+
+
+def step_p2p(T, source, target, dmax, grid: Grid | None = None):
+    """Point-to-point pass at fixed T: corr and the 29 p2p terms
+    ([0..8] sum s'q^T, [9..11] sum s', [12..14] sum q, [27] count, [28] sum d2)."""
+    src, tgt = _f32(source), _f32(target)
+    corr = np.empty(len(src), np.int32)
+    sums = np.zeros(NTERMS)
+    lib().orc_pass_p2p(_p(_f64(T)), _p(src), len(src), _p(tgt), len(tgt),
+                       grid.h if grid is not None else None, float(dmax), _p(corr), _p(sums))
+    return dict(corr=corr, terms=sums, count=sums[27], sum_sq_dist=sums[28])
+
+
+def kabsch(terms):
+    """Rigid transform from p2p terms, or None if degenerate."""
+    T = np.zeros(16)
+    rc = lib().orc_kabsch(_p(_f64(terms)), _p(T))
+    return None if rc else T.reshape(4, 4)
+
+
+def icp_p2p(source, target, dmax, max_iterations, init_T=None, relative_fitness=1e-6,
+            relative_rmse=1e-6):
+    """registration_icp with TransformationEstimationPointToPoint(False)."""
+    src, tgt = _f32(source), _f32(target)
+    T0 = _f64(np.eye(4) if init_T is None else init_T)
+    T = np.zeros(16)
+    fit, rmse = np.zeros(1), np.zeros(1)
+    it, fl, cv = np.zeros(1, np.int32), np.zeros(1, np.int32), np.zeros(1, np.int32)
+    passes = lib().orc_icp_p2p(_p(src), len(src), _p(tgt), len(tgt), _p(T0), float(dmax),
+                               int(max_iterations), float(relative_fitness), float(relative_rmse),
+                               _p(T), _p(fit), _p(rmse), _p(it), _p(fl), _p(cv))
+    if passes < 0:
+        raise MemoryError("oracle icp_p2p failed")
+    return dict(T=T.reshape(4, 4), fitness=float(fit[0]), inlier_rmse=float(rmse[0]),
+                iterations=int(it[0]), flags=int(fl[0]), converged=bool(cv[0]), passes=passes)

@@ -505,3 +505,176 @@ int orc_icp_multiscale(const float *src, int64_t n, const float *tgt, const floa
     free(sp); free(tp); free(tn);
     return 0;
 }
+
+/* ------------------------------------------ point-to-point ICP (NEXT 2) */
+/* TransformationEstimationPointToPoint(False) ("Other ICP variants
+ * are implemented as well" P:212): closed-form rigid fit
+ * minimising sum |R s'_i + t - q_i|^2 over the correspondences, no scale,
+ * reflection corrected so det R = +1 (Kabsch/SVD). The 29 terms of a pass:
+ * [0..8] sum s'_a q_b (row-major a,b), [9..11] sum s', [12..14] sum q,
+ * [27] count, [28] sum d^2; the correspondence rule is the same as above. */
+static void record_p2p(const double s[3], const float *qf, double d2, acc_t acc[ORC_NTERMS])
+{
+    double q[3] = {(double)qf[0], (double)qf[1], (double)qf[2]};
+    for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b) acc_add(&acc[3 * a + b], s[a] * q[b]);
+    for (int a = 0; a < 3; ++a) acc_add(&acc[9 + a], s[a]);
+    for (int a = 0; a < 3; ++a) acc_add(&acc[12 + a], q[a]);
+    acc_add(&acc[27], 1.0);
+    acc_add(&acc[28], d2);
+}
+
+void orc_pass_p2p(const double T[16], const float *src, int64_t n, const float *tgt, int64_t m,
+                  const orc_grid *g, double dmax, int32_t *corr, double *sums)
+{
+    acc_t acc[ORC_NTERMS];
+    memset(acc, 0, sizeof(acc));
+    const double r2 = dmax * dmax;
+    for (int64_t i = 0; i < n; ++i) {
+        double s[3], d2 = 0.0;
+        orc_transform_point(T, src + 3 * i, s);
+        int64_t j = g ? orc_nn_grid(g, s, r2, &d2) : orc_nn_brute(s, tgt, m, r2, &d2);
+        if (corr) corr[i] = (int32_t)j;
+        if (j >= 0) record_p2p(s, tgt + 3 * j, d2, acc);
+    }
+    for (int t = 0; t < ORC_NTERMS; ++t) sums[t] = acc[t].s + acc[t].c;
+}
+
+/* Jacobi eigen-decomposition of a symmetric 3x3 A (destroyed): eigenvalues
+ * in w, eigenvectors in the columns of V (row-major).                     */
+static void jacobi3(double A[9], double w[3], double V[9])
+{
+    for (int i = 0; i < 9; ++i) V[i] = (i % 4 == 0) ? 1.0 : 0.0;
+    for (int sweep = 0; sweep < 64; ++sweep) {
+        double off = fabs(A[1]) + fabs(A[2]) + fabs(A[5]);
+        double dia = fabs(A[0]) + fabs(A[4]) + fabs(A[8]);
+        if (off <= 1e-300 || off <= 1e-18 * dia) break;
+        for (int p = 0; p < 2; ++p)
+            for (int q = p + 1; q < 3; ++q) {
+                double apq = A[3 * p + q];
+                if (apq == 0.0) continue;
+                double theta = (A[3 * q + q] - A[3 * p + p]) / (2.0 * apq);
+                double t = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
+                double c = 1.0 / sqrt(t * t + 1.0), s = t * c;
+                for (int k = 0; k < 3; ++k) {   /* A <- J^T A J */
+                    double akp = A[3 * k + p], akq = A[3 * k + q];
+                    A[3 * k + p] = c * akp - s * akq;
+                    A[3 * k + q] = s * akp + c * akq;
+                }
+                for (int k = 0; k < 3; ++k) {
+                    double apk = A[3 * p + k], aqk = A[3 * q + k];
+                    A[3 * p + k] = c * apk - s * aqk;
+                    A[3 * q + k] = s * apk + c * aqk;
+                }
+                for (int k = 0; k < 3; ++k) {
+                    double vkp = V[3 * k + p], vkq = V[3 * k + q];
+                    V[3 * k + p] = c * vkp - s * vkq;
+                    V[3 * k + q] = s * vkp + c * vkq;
+                }
+            }
+    }
+    for (int i = 0; i < 3; ++i) w[i] = A[4 * i];
+}
+
+/* Kabsch: R, t minimising sum |R s + t - q|^2 from the p2p terms. Returns 0,
+ * or 1 if degenerate (count < 3 or rank(H) < 2: sigma_2 <= 1e-6 sigma_1, R15).
+ * H = sum s q^T - n mu_s mu_q^T = U S V^T  ->  R = V diag(1,1,d) U^T,
+ * d = sign det(V U^T); t = mu_q - R mu_s.                                  */
+int orc_kabsch(const double *terms, double Tout[16])
+{
+    const double cnt = terms[27];
+    if (!(cnt >= 3.0)) return 1;
+    double ms[3], mq[3], H[9];
+    for (int a = 0; a < 3; ++a) { ms[a] = terms[9 + a] / cnt; mq[a] = terms[12 + a] / cnt; }
+    for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b) H[3 * a + b] = terms[3 * a + b] - cnt * ms[a] * mq[b];
+    double HtH[9], w[3], V[9];
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) {
+            double s = 0.0;
+            for (int k = 0; k < 3; ++k) s += H[3 * k + i] * H[3 * k + j];
+            HtH[3 * i + j] = s;
+        }
+    jacobi3(HtH, w, V);
+    int order[3] = {0, 1, 2};   /* sort eigenpairs descending */
+    for (int i = 0; i < 3; ++i)
+        for (int j = i + 1; j < 3; ++j)
+            if (w[order[j]] > w[order[i]]) { int tmp = order[i]; order[i] = order[j]; order[j] = tmp; }
+    double sig[3], Vs[9], U[9];
+    for (int c = 0; c < 3; ++c) {
+        sig[c] = sqrt(w[order[c]] > 0.0 ? w[order[c]] : 0.0);
+        for (int r = 0; r < 3; ++r) Vs[3 * r + c] = V[3 * r + order[c]];
+    }
+    if (!(sig[0] > 0.0) || !(sig[1] > 1e-6 * sig[0])) return 1;   /* R15: sigma via H^T H */
+    for (int c = 0; c < 2; ++c)          /* U_c = H V_c / sigma_c */
+        for (int r = 0; r < 3; ++r) {
+            double s = 0.0;
+            for (int k = 0; k < 3; ++k) s += H[3 * r + k] * Vs[3 * k + c];
+            U[3 * r + c] = s / sig[c];
+        }
+    U[2] = U[3] * U[7] - U[6] * U[4];    /* U_2 = U_0 x U_1 */
+    U[5] = U[6] * U[1] - U[0] * U[7];
+    U[8] = U[0] * U[4] - U[3] * U[1];
+    double R[9];                         /* R = V diag(1,1,d) U^T, det(R) = +1 */
+    for (int pass = 0; pass < 2; ++pass) {
+        double d = pass == 0 ? 1.0 : -1.0;
+        for (int i = 0; i < 3; ++i)
+            for (int j = 0; j < 3; ++j)
+                R[3 * i + j] = Vs[3 * i + 0] * U[3 * j + 0] + Vs[3 * i + 1] * U[3 * j + 1] +
+                               d * Vs[3 * i + 2] * U[3 * j + 2];
+        double det = R[0] * (R[4] * R[8] - R[5] * R[7]) - R[1] * (R[3] * R[8] - R[5] * R[6]) +
+                     R[2] * (R[3] * R[7] - R[4] * R[6]);
+        if (det > 0.0) break;
+    }
+    memset(Tout, 0, 16 * sizeof(double));
+    for (int i = 0; i < 3; ++i) {
+        for (int j = 0; j < 3; ++j) Tout[4 * i + j] = R[3 * i + j];
+        Tout[4 * i + 3] = mq[i] - (R[3 * i] * ms[0] + R[3 * i + 1] * ms[1] + R[3 * i + 2] * ms[2]);
+    }
+    Tout[15] = 1.0;
+    return 0;
+}
+
+/* registration_icp with TransformationEstimationPointToPoint(False): the
+ * same loop, criteria and flags as orc_icp, with the Kabsch
+ * update T <- T_est T.                                                    */
+int orc_icp_p2p(const float *src, int64_t n, const float *tgt, int64_t m, const double T0[16],
+                double dmax, int32_t max_iterations, double relative_fitness, double relative_rmse,
+                double T_out[16], double *fitness, double *inlier_rmse, int32_t *iterations,
+                int32_t *flags, int32_t *converged)
+{
+    orc_grid *g = orc_grid_build(tgt, m, dmax);
+    if (!g) return -1;
+    double T[16], sums[ORC_NTERMS];
+    memcpy(T, T0, sizeof(T));
+    int32_t it = 0, fl = 0, conv = 0, passes = 0;
+    orc_pass_p2p(T, src, n, tgt, m, g, dmax, NULL, sums);
+    double cnt = sums[27];
+    double fit = cnt / (double)n, rmse = cnt > 0 ? sqrt(sums[28] / cnt) : 0.0;
+    ++passes;
+    double fp = fit, rp = rmse;
+    while (it < max_iterations) {
+        if (cnt == 0.0) { fl |= ORC_FLAG_NO_CORR; break; }
+        double dT[16];
+        if (orc_kabsch(sums, dT)) { fl |= ORC_FLAG_DEGENERATE; break; }
+        orc_compose(dT, T, T);
+        ++it;
+        orc_pass_p2p(T, src, n, tgt, m, g, dmax, NULL, sums);
+        cnt = sums[27];
+        fit = cnt / (double)n;
+        rmse = cnt > 0 ? sqrt(sums[28] / cnt) : 0.0;
+        ++passes;
+        if (fabs(fit - fp) < relative_fitness && fabs(rmse - rp) < relative_rmse) { conv = 1; break; }
+        fp = fit;
+        rp = rmse;
+    }
+    if (cnt == 0.0) fl |= ORC_FLAG_NO_CORR;
+    memcpy(T_out, T, sizeof(T));
+    *fitness = fit;
+    *inlier_rmse = rmse;
+    *iterations = it;
+    *flags = fl;
+    *converged = conv;
+    orc_grid_free(g);
+    return passes;
+}

@@ -384,3 +384,71 @@ def test_multiscale_recovers_motion():
     src = apply(M, tgt.astype(np.float64)).astype(np.float32)
     ms = oracle.icp_multiscale(src, tgt, nrm, [0.08, 0.04, 0.02], [0.16, 0.08, 0.04], [30, 20, 10])
     assert np.abs(ms["T"] - inv_rigid(M)).max() < 2e-3
+
+
+# ----------------------------------------------- point-to-point ICP (NEXT 2)
+def _kabsch_numpy(s, q):
+    """Textbook Kabsch via numpy's SVD (an independent library route)."""
+    ms, mq = s.mean(0), q.mean(0)
+    H = (s - ms).T @ (q - mq)
+    U, S, Vt = np.linalg.svd(H)
+    d = np.sign(np.linalg.det(Vt.T @ U.T))
+    R = Vt.T @ np.diag([1, 1, d]) @ U.T
+    return rigid(R, mq - R @ ms)
+
+
+def test_kabsch_matches_numpy_svd_and_exact_motion():
+    rs = Stream(505)
+    for _ in range(20):
+        s = rs.uniform(300, -2, 2).reshape(-1, 3)
+        M = _rand_T(rs, 1.0, 1.0)
+        q = apply(M, s) + 0.01 * rs.uniform(300, -1, 1).reshape(-1, 3)
+        terms = np.zeros(29)
+        terms[0:9] = (s[:, :, None] * q[:, None, :]).sum(0).ravel()
+        terms[9:12], terms[12:15], terms[27] = s.sum(0), q.sum(0), len(s)
+        T = oracle.kabsch(terms)
+        assert np.abs(T - _kabsch_numpy(s, q)).max() < 1e-9
+        assert abs(np.linalg.det(T[:3, :3]) - 1) < 1e-12
+    # exact motion recovered (S:259 "recovers R,t within 1e-10")
+    s = rs.uniform(600, -1, 1).reshape(-1, 3)
+    M = _rand_T(rs, 0.7, 0.5)
+    q = apply(M, s)
+    terms = np.zeros(29)
+    terms[0:9] = (s[:, :, None] * q[:, None, :]).sum(0).ravel()
+    terms[9:12], terms[12:15], terms[27] = s.sum(0), q.sum(0), len(s)
+    assert np.abs(oracle.kabsch(terms) - M).max() < 1e-10
+
+
+def test_kabsch_reflection_and_degenerate():
+    rs = Stream(506)
+    s = rs.uniform(300, -1, 1).reshape(-1, 3)
+    q = s * np.array([1, 1, -1])                      # a mirror: best proper rotation, det +1
+    terms = np.zeros(29)
+    terms[0:9] = (s[:, :, None] * q[:, None, :]).sum(0).ravel()
+    terms[9:12], terms[12:15], terms[27] = s.sum(0), q.sum(0), len(s)
+    T = oracle.kabsch(terms)
+    assert abs(np.linalg.det(T[:3, :3]) - 1) < 1e-12
+    assert np.abs(T - _kabsch_numpy(s, q)).max() < 1e-9
+    line = np.outer(np.linspace(-1, 1, 50), [1.0, 2.0, 3.0])   # collinear: rank(H) = 1
+    terms = np.zeros(29)
+    terms[0:9] = (line[:, :, None] * line[:, None, :]).sum(0).ravel()
+    terms[9:12], terms[12:15], terms[27] = line.sum(0), line.sum(0), len(line)
+    assert oracle.kabsch(terms) is None
+    terms[27] = 2.0
+    assert oracle.kabsch(terms) is None
+
+
+def test_icp_p2p_recovers_motion():
+    """5 deg + 0.02 perturbation -> rotation error < 0.1 deg,
+    translation error < 1e-3 (here noise-free twins, well conditioned)."""
+    rs = Stream(507)
+    tgt, _ = _scene_small(rs, 4000)
+    tgt = tgt.astype(np.float32)
+    M = rigid(rotation([0.3, -0.2, 1.0], math.radians(5.0)), [0.02, -0.01, 0.015])
+    src = apply(M, tgt.astype(np.float64)).astype(np.float32)
+    r = oracle.icp_p2p(src, tgt, 0.3, 60)
+    E = r["T"] @ M
+    ang = math.degrees(math.acos(min(1.0, (np.trace(E[:3, :3]) - 1) / 2)))
+    assert ang < 0.1 and np.abs(E[:3, 3]).max() < 1e-3
+    r = oracle.icp_p2p(tgt, tgt, 0.05, 10)            # S:288 fixed point
+    assert np.abs(r["T"] - np.eye(4)).max() < 1e-12 and r["fitness"] == 1.0

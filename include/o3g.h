@@ -98,6 +98,16 @@ o3g_status o3g_icp_point_to_plane(const float* source_xyz, int64_t n_source,
                                   double* fitness, double* inlier_rmse, o3g_icp_info* info,
                                   void* cuda_stream);
 
+/* registration_icp with TransformationEstimationPointToPoint(False)
+ * (SPEC S:255-263): same arguments, loop,
+ * criteria, flags and return values as o3g_icp_point_to_plane, no normals. */
+o3g_status o3g_icp_point_to_point(const float* source_xyz, int64_t n_source,
+                                  const float* target_xyz, int64_t n_target,
+                                  const double init_T[16], double max_correspondence_distance,
+                                  int32_t max_iterations, double relative_fitness,
+                                  double relative_rmse, double T_out[16], double* fitness,
+                                  double* inlier_rmse, o3g_icp_info* info, void* cuda_stream);
+
 /* --------------------------------------------------------------- stateful */
 /* Create a context on CUDA device `device`, ordered on `cuda_stream`.     */
 o3g_status o3g_create(o3g_ctx** out, int device, void* cuda_stream);
@@ -105,7 +115,8 @@ o3g_status o3g_destroy(o3g_ctx* ctx);
 
 /* A1: build the voxel-hash grid over the target (cell size
  * dmax*(1+2^-20)); keeps sorted float4 copies of xyz (+ original index)
- * and normals. Invalidates any previously set source ordering.          */
+ * and normals. normals may be NULL only for point-to-point estimation.
+ * Invalidates any previously set source ordering.                       */
 o3g_status o3g_set_target(o3g_ctx* ctx, const float* xyz, const float* normals, int64_t n,
                           double max_correspondence_distance);
 
@@ -192,9 +203,16 @@ o3g_status o3g_dist_init(o3g_ctx* ctx, int rank, int world, const void* nccl_uni
  * O3G_OPT_COOP_MIN: variant 1 scans a query with at least this many
  *   candidates with the whole warp (0 = never; -1 = auto, the default:
  *   256 when the target averages >= 32 points per occupied cell, else 0).
- * Results are identical for every option value.                         */
+ * O3G_OPT_ESTIMATION: 0 = point-to-plane (default), 1 = point-to-point
+ *   (TransformationEstimationPointToPoint(False); SPEC
+ *   S:255-263): Horn's closed-form rigid fit on the correspondences, no
+ *   scale, det R = +1; degenerate if < 3 pairs or rank(H) < 2 (R15). The
+ *   29 terms of o3g_icp_step then hold [0..8] sum s'q^T (row-major),
+ *   [9..11] sum s', [12..14] sum q, [27] count, [28] sum d^2 (JTJ/JTr
+ *   outputs carry the same raw slots). Target normals are then optional.
+ * Results are identical for every value of the other options.           */
 enum { O3G_OPT_SEARCH = 1, O3G_OPT_GRID = 2, O3G_OPT_TIMING = 3, O3G_OPT_BLOCKS_PER_SM = 4,
-       O3G_OPT_NBR_MASK = 5, O3G_OPT_COOP_MIN = 6 };
+       O3G_OPT_NBR_MASK = 5, O3G_OPT_COOP_MIN = 6, O3G_OPT_ESTIMATION = 7 };
 o3g_status o3g_set_option(o3g_ctx* ctx, int option, int64_t value);
 
 /* Sum of the correspondence-kernel (K3) durations of the last o3g_icp_run

@@ -97,7 +97,8 @@ __global__ void k_gather_target(const float* __restrict__ xyz, const float* __re
         int32_t v = vals[i];
         tpos[i] = make_float4(xyz[3 * (int64_t)v], xyz[3 * (int64_t)v + 1], xyz[3 * (int64_t)v + 2],
                               __int_as_float(v));
-        tnrm[i] = make_float4(nrm[3 * (int64_t)v], nrm[3 * (int64_t)v + 1], nrm[3 * (int64_t)v + 2], 0.f);
+        tnrm[i] = nrm ? make_float4(nrm[3 * (int64_t)v], nrm[3 * (int64_t)v + 1], nrm[3 * (int64_t)v + 2], 0.f)
+                      : make_float4(0.f, 0.f, 0.f, 0.f);
         occ += (i == 0 || keys[i] != keys[i - 1]);
     }
     for (int o = 16; o; o >>= 1) occ += __shfl_xor_sync(0xffffffffu, occ, o);

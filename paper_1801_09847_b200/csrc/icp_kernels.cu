@@ -465,7 +465,13 @@ __global__ void __launch_bounds__(kK3Threads, 4) k3_balanced(const K3Args a) {
         const unsigned matched = __ballot_sync(0xffffffffu, win >= 0);
         if (matched) {
             double v[8] = {0, 0, 0, 0, 0, 0, 0, 0}, d2w = 0.0;
-            if (win >= 0) {
+            if (win >= 0 && a.p2p) {
+                // point-to-point record, staged as rows 0-3 (s', 1) and 4-6 (q)
+                v[0] = sx, v[1] = sy, v[2] = sz, v[3] = 1.0;
+                v[4] = wq.x, v[5] = wq.y, v[6] = wq.z;
+                v[7] = 0.0;
+                d2w = wd2;
+            } else if (win >= 0) {
                 const float4 nf = __ldg(&a.tnrm[win]);
                 const double nx = nf.x, ny = nf.y, nz = nf.z;
                 v[0] = sy * nz - sz * ny;
@@ -481,12 +487,19 @@ __global__ void __launch_bounds__(kK3Threads, 4) k3_balanced(const K3Args a) {
             vw[8 * kVW + lane] = d2w;
             __syncwarp();
             // A6: C += V^T W over the 32 records, 4 records per mma (fixed order)
-            // V rows (J0..J5, r, m) = 0..7; W rows (J0..J5, m, d2) = 0..5, 7, 8
-            const int row = lane >> 2, kk = lane & 3, wrow = row < 6 ? row : row + 1;
+            // plane: V rows (J0..J5, r, m) = 0..7; W rows (J0..J5, m, d2) = 0..5, 7, 8.
+            // point: V = (s'x, s'y, s'z, 1, 0..) = rows 0-3 then zero row 7;
+            //        W = (qx, qy, qz, 1, d2, 0..) = rows 4, 5, 6, 3, 8 then row 7, so
+            //        C[a][b] = sum s'_a q_b, C[a][3] = sum s'_a, C[3][b] = sum q_b,
+            //        C[3][3] = count, C[3][4] = sum d2 (term_cidx_p2p)
+            const int row = lane >> 2, kk = lane & 3;
+            const int wrow = a.p2p ? (row < 3 ? row + 4 : row == 3 ? 3 : row == 4 ? 8 : 7)
+                                   : (row < 6 ? row : row + 1);
+            const int vrow = a.p2p ? (row < 4 ? row : 7) : row;
 #pragma unroll
             for (int c4 = 0; c4 < 8; ++c4) {
                 if ((matched >> (4 * c4)) & 0xFu)
-                    dmma884(acc0, acc1, vw[row * kVW + 4 * c4 + kk], vw[wrow * kVW + 4 * c4 + kk]);
+                    dmma884(acc0, acc1, vw[vrow * kVW + 4 * c4 + kk], vw[wrow * kVW + 4 * c4 + kk]);
             }
             __syncwarp();
         }
@@ -497,10 +510,10 @@ __global__ void __launch_bounds__(kK3Threads, 4) k3_balanced(const K3Args a) {
     __syncthreads();
     if (threadIdx.x < kTermStride) {
         double s = 0.0;
-        if (threadIdx.x < kTerms) {
-            const int ci = term_cidx(threadIdx.x);
+        const int ci = a.p2p ? term_cidx_p2p(threadIdx.x)
+                             : (threadIdx.x < kTerms ? term_cidx(threadIdx.x) : -1);
+        if (ci >= 0)
             for (int w = 0; w < kK3Threads / 32; ++w) s += red[w][ci];
-        }
         a.block_partials[(size_t)blockIdx.x * kTermStride + threadIdx.x] = s;
     }
     if (!a.fuse_mode) return;
@@ -647,6 +660,93 @@ __device__ static void se3_exp(const double* xi, double* E /*3x4*/) {
     }
 }
 
+// Symmetric Jacobi eigen-decomposition (cyclic sweeps), n <= 4, row-major.
+template <int N>
+__device__ static void sym_eig(double* A, double* w, double* V) {
+    for (int i = 0; i < N * N; ++i) V[i] = (i % (N + 1) == 0) ? 1.0 : 0.0;
+    for (int sweep = 0; sweep < 64; ++sweep) {
+        double off = 0.0, dia = 0.0;
+        for (int i = 0; i < N; ++i) {
+            dia += fabs(A[i * N + i]);
+            for (int j = i + 1; j < N; ++j) off += fabs(A[i * N + j]);
+        }
+        if (off <= 1e-300 || off <= 1e-18 * dia) break;
+        for (int p = 0; p < N - 1; ++p)
+            for (int q = p + 1; q < N; ++q) {
+                const double apq = A[p * N + q];
+                if (apq == 0.0) continue;
+                const double th = (A[q * N + q] - A[p * N + p]) / (2.0 * apq);
+                const double t = (th >= 0 ? 1.0 : -1.0) / (fabs(th) + sqrt(th * th + 1.0));
+                const double c = 1.0 / sqrt(t * t + 1.0), sn = t * c;
+                for (int k = 0; k < N; ++k) {
+                    const double akp = A[k * N + p], akq = A[k * N + q];
+                    A[k * N + p] = c * akp - sn * akq;
+                    A[k * N + q] = sn * akp + c * akq;
+                }
+                for (int k = 0; k < N; ++k) {
+                    const double apk = A[p * N + k], aqk = A[q * N + k];
+                    A[p * N + k] = c * apk - sn * aqk;
+                    A[q * N + k] = sn * apk + c * aqk;
+                }
+                for (int k = 0; k < N; ++k) {
+                    const double vkp = V[k * N + p], vkq = V[k * N + q];
+                    V[k * N + p] = c * vkp - sn * vkq;
+                    V[k * N + q] = sn * vkp + c * vkq;
+                }
+            }
+    }
+    for (int i = 0; i < N; ++i) w[i] = A[i * N + i];
+}
+
+// Point-to-point estimation (TransformationEstimationPointToPoint(False),
+// P:193): the rigid (R, t) minimising sum |R s' + t - q|^2
+// by Horn's unit-quaternion method (the top eigenvector of the 4x4 matrix N
+// built from H = sum s'q^T - n mu_s mu_q^T always yields det R = +1).
+// Degenerate (false) if count < 3 or rank(H) < 2, i.e. sigma_2 <= 1e-6
+// sigma_1 from the eigenvalues of H^T H (R15). E: 3x4 [R | t].
+__device__ static bool horn_fit(const double* terms, double* E) {
+    const double cnt = terms[27];
+    if (!(cnt >= 3.0)) return false;
+    double ms[3], mq[3], S[9];
+    for (int a = 0; a < 3; ++a) ms[a] = terms[9 + a] / cnt, mq[a] = terms[12 + a] / cnt;
+    for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b) S[3 * a + b] = terms[3 * a + b] - cnt * ms[a] * mq[b];
+    double G[9], gw[3], gv[9];
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j)
+            G[3 * i + j] = S[i] * S[j] + S[3 + i] * S[3 + j] + S[6 + i] * S[6 + j];
+    sym_eig<3>(G, gw, gv);
+    double e0 = fmax(gw[0], 0.0), e1 = fmax(gw[1], 0.0), e2 = fmax(gw[2], 0.0);
+    const double hi = fmax(e0, fmax(e1, e2)), lo = fmin(e0, fmin(e1, e2));
+    const double mid = e0 + e1 + e2 - hi - lo;
+    if (!(hi > 0.0) || !(sqrt(mid) > 1e-6 * sqrt(hi))) return false;
+    const double Sxx = S[0], Sxy = S[1], Sxz = S[2], Syx = S[3], Syy = S[4], Syz = S[5], Szx = S[6],
+                 Szy = S[7], Szz = S[8];
+    double N[16] = {Sxx + Syy + Szz, Syz - Szy,        Szx - Sxz,        Sxy - Syx,
+                    Syz - Szy,       Sxx - Syy - Szz,  Sxy + Syx,        Szx + Sxz,
+                    Szx - Sxz,       Sxy + Syx,        -Sxx + Syy - Szz, Syz + Szy,
+                    Sxy - Syx,       Szx + Sxz,        Syz + Szy,        -Sxx - Syy + Szz};
+    double nw[4], nv[16];
+    sym_eig<4>(N, nw, nv);
+    int k = 0;
+    for (int i = 1; i < 4; ++i)
+        if (nw[i] > nw[k]) k = i;
+    double q0 = nv[k], qx = nv[4 + k], qy = nv[8 + k], qz = nv[12 + k];
+    const double qn = sqrt(q0 * q0 + qx * qx + qy * qy + qz * qz);
+    q0 /= qn, qx /= qn, qy /= qn, qz /= qn;
+    const double R[9] = {q0 * q0 + qx * qx - qy * qy - qz * qz, 2.0 * (qx * qy - q0 * qz),
+                         2.0 * (qx * qz + q0 * qy),
+                         2.0 * (qy * qx + q0 * qz), q0 * q0 - qx * qx + qy * qy - qz * qz,
+                         2.0 * (qy * qz - q0 * qx),
+                         2.0 * (qz * qx - q0 * qy), 2.0 * (qz * qy + q0 * qx),
+                         q0 * q0 - qx * qx - qy * qy + qz * qz};
+    for (int i = 0; i < 3; ++i) {
+        for (int j = 0; j < 3; ++j) E[4 * i + j] = R[3 * i + j];
+        E[4 * i + 3] = mq[i] - (R[3 * i] * ms[0] + R[3 * i + 1] * ms[1] + R[3 * i + 2] * ms[2]);
+    }
+    return true;
+}
+
 // Thread-0 epilogue of a pass (A8): store the 29 terms; in SOLVE mode apply the
 // criteria (R7, R8) and the Gauss-Newton update (Eq. 2, R5, R6) to the state.
 __device__ __noinline__ void tail_finish(const double* terms, IcpState* st, double* hist_fit, double* hist_rmse,
@@ -676,6 +776,20 @@ __device__ __noinline__ void tail_finish(const double* terms, IcpState* st, doub
     if (!done) {
         if (st->it >= st->max_it || cnt == 0.0) {
             done = 1;
+        } else if (mode & TAIL_P2P) {
+            double E[12], Tn[12];
+            if (!horn_fit(terms, E)) {
+                st->flags |= 2;  // O3G_FLAG_DEGENERATE
+                done = 1;
+            } else {
+                for (int i = 0; i < 3; ++i)
+                    for (int j = 0; j < 4; ++j)
+                        Tn[4 * i + j] = E[4 * i + 0] * st->T[j] + E[4 * i + 1] * st->T[4 + j] +
+                                        E[4 * i + 2] * st->T[8 + j] + (j == 3 ? E[4 * i + 3] : 0.0);
+                for (int q = 0; q < 12; ++q) st->T[q] = Tn[q];
+                st->T[12] = 0.0, st->T[13] = 0.0, st->T[14] = 0.0, st->T[15] = 1.0;
+                st->it += 1;
+            }
         } else {
             double A[36], b[6], xi[6];
             int k = 0;

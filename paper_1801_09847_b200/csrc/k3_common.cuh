@@ -39,4 +39,16 @@ __device__ __forceinline__ int term_cidx(int t) {
     return t == 27 ? 7 * 8 + 6 : 7 * 8 + 7;
 }
 
+// point-to-point term t -> flat C index (-1 = unused slot, stays 0):
+// [0..8] sum s'_a q_b = C[a][b], [9..11] sum s' = C[a][3], [12..14] sum q =
+// C[3][b], [27] count = C[3][3], [28] sum d2 = C[3][4]
+__device__ __forceinline__ int term_cidx_p2p(int t) {
+    if (t < 9) return (t / 3) * 8 + (t % 3);
+    if (t < 12) return (t - 9) * 8 + 3;
+    if (t < 15) return 3 * 8 + (t - 12);
+    if (t == 27) return 3 * 8 + 3;
+    if (t == 28) return 3 * 8 + 4;
+    return -1;
+}
+
 }  // namespace o3g

@@ -120,6 +120,8 @@ struct o3g_ctx {
 
     // options
     int search = 1, grid_mode = 0, timing = 0, bps_override = 0, nbr_mask = 1, coop_min = -1;
+    int estimation = 0;   // 0 point-to-plane, 1 point-to-point
+    bool has_normals = false;
 
     // target grid
     int64_t m = 0;
@@ -309,6 +311,10 @@ o3g_status o3g_set_option(o3g_ctx* c, int option, int64_t value) {
             break;
         case O3G_OPT_TIMING: c->timing = value ? 1 : 0; break;
         case O3G_OPT_NBR_MASK: c->nbr_mask = value ? 1 : 0; break;
+        case O3G_OPT_ESTIMATION:
+            if (value < 0 || value > 1) return fail(O3G_ERR_INVALID_ARGUMENT, "estimation must be 0 or 1");
+            c->estimation = (int)value;
+            break;
         case O3G_OPT_COOP_MIN:
             if (value < -1 || value > (1 << 30)) return fail(O3G_ERR_INVALID_ARGUMENT, "coop_min out of range");
             c->coop_min = (int)value;
@@ -326,7 +332,7 @@ o3g_status o3g_set_option(o3g_ctx* c, int option, int64_t value) {
 o3g_status o3g_set_target(o3g_ctx* c, const float* xyz, const float* normals, int64_t n,
                           double dmax) {
     if (!c) return fail(O3G_ERR_INVALID_ARGUMENT, "ctx is NULL");
-    if (!xyz || !normals) return fail(O3G_ERR_INVALID_ARGUMENT, "target xyz and normals are required");
+    if (!xyz) return fail(O3G_ERR_INVALID_ARGUMENT, "target xyz is required");
     if (n <= 0 || n > 0x7ffffffeLL) return fail(O3G_ERR_INVALID_ARGUMENT, "n_target must be in [1, 2^31-2]");
     if (!(dmax > 0.0) || !isfinite(dmax)) return fail(O3G_ERR_INVALID_ARGUMENT, "max_correspondence_distance must be finite and > 0");
     TRY(enter(c));
@@ -335,7 +341,8 @@ o3g_status o3g_set_target(o3g_ctx* c, const float* xyz, const float* normals, in
     invalidate_graph(c);
     const float *dx, *dn;
     TRY(device_view(c, xyz, 3 * n, c->stage_a, &dx));
-    TRY(device_view(c, normals, 3 * n, c->stage_b, &dn));
+    dn = nullptr;
+    if (normals) TRY(device_view(c, normals, 3 * n, c->stage_b, &dn));
 
     // A0/A1: bbox + finiteness (one sync: the grid dims size the table)
     TRY(c->misc.ensure(64));
@@ -346,8 +353,8 @@ o3g_status o3g_set_target(o3g_ctx* c, const float* xyz, const float* normals, in
     CK(cudaMemsetAsync(mm + 3, 0x00, 12 + 4 + 4 + 8, c->exec));
     CK(cudaMemsetAsync(mm + 12, 0x00, 4, c->exec));   // fused-tail block counter
     launch_bbox(dx, n, mm, bad, c->sms, c->exec);
-    launch_check_finite(dn, 3 * n, bad, c->sms, c->exec);
-    c->launches += 2;
+    if (dn) launch_check_finite(dn, 3 * n, bad, c->sms, c->exec);
+    c->launches += dn ? 2 : 1;
     uint32_t h[8];
     CK(cudaMemcpyAsync(h, mm, 32, cudaMemcpyDeviceToHost, c->exec));
     CK(cudaStreamSynchronize(c->exec));
@@ -421,6 +428,7 @@ o3g_status o3g_set_target(o3g_ctx* c, const float* xyz, const float* normals, in
     c->g = g;
     c->m = n;
     c->dmax = dmax;
+    c->has_normals = dn != nullptr;
     c->occupied = (int64_t)h_occ;
     return O3G_OK;
 }
@@ -467,10 +475,12 @@ o3g_status o3g_set_source(o3g_ctx* c, const float* xyz, int64_t n, const double 
     return O3G_OK;
 }
 
+static int k3_variant(const o3g_ctx* c) { return c->estimation ? 1 : c->search; }
+
 static int k3_blocks(o3g_ctx* c, bool write_corr) {
-    int bps = c->bps_override ? c->bps_override : k3_max_blocks_per_sm(c->search, write_corr, c->g.hashed);
+    int bps = c->bps_override ? c->bps_override : k3_max_blocks_per_sm(k3_variant(c), write_corr, c->g.hashed);
     if (bps < 1) bps = 1;
-    const int tpb = k3_threads(c->search);
+    const int tpb = k3_threads(k3_variant(c));
     int64_t need = (c->n_local + tpb - 1) / tpb;
     int64_t b = (int64_t)c->sms * bps;
     if (need < b) b = need;
@@ -503,6 +513,7 @@ static K3Args k3_args(o3g_ctx* c, int32_t* corr) {
     a.nbr_bits = (c->nbr_mask && c->nbr_ready) ? c->nbr_a.as<uint32_t>() : nullptr;
     // auto (-1): warp-cooperative scans only where cells are dense (measured:
     // LiDAR, 226 points per occupied cell, gains 1.6x; sparse configs lose)
+    a.p2p = c->estimation;
     a.coop_min = c->coop_min >= 0 ? c->coop_min
                                   : ((double)c->m >= 32.0 * (double)(c->occupied > 0 ? c->occupied : 1) ? 256 : 0);
     a.fuse_mode = 0;
@@ -516,7 +527,8 @@ static K3Args k3_args(o3g_ctx* c, int32_t* corr) {
 static o3g_status enqueue_pass(o3g_ctx* c, int blocks, bool write_corr, int32_t* corr,
                                int tail_mode, cudaEvent_t ev0, cudaEvent_t ev1, int* nlaunch) {
     if (ev0) CK(cudaEventRecordWithFlags(ev0, c->exec, cudaEventRecordExternal));
-    const bool fused = c->world == 1 && c->search == 1 && c->n_local > 0;
+    const bool fused = c->world == 1 && k3_variant(c) == 1 && c->n_local > 0;
+    if (c->estimation) tail_mode |= TAIL_P2P;
     if (c->n_local > 0) {
         K3Args ka = k3_args(c, corr);
         if (fused) {
@@ -526,7 +538,7 @@ static o3g_status enqueue_pass(o3g_ctx* c, int blocks, bool write_corr, int32_t*
             ka.hist_fit = c->hist_fit.as<double>();
             ka.hist_rmse = c->hist_rmse.as<double>();
         }
-        launch_k3(ka, blocks, c->search, write_corr, c->exec);
+        launch_k3(ka, blocks, k3_variant(c), write_corr, c->exec);
         ++*nlaunch;
     }
     if (ev1) CK(cudaEventRecordWithFlags(ev1, c->exec, cudaEventRecordExternal));
@@ -570,6 +582,7 @@ o3g_status o3g_icp_step(o3g_ctx* c, const double T_in[16], int32_t* corr_out, do
     if (!c) return fail(O3G_ERR_INVALID_ARGUMENT, "ctx is NULL");
     if (!rigid_ok(T_in)) return fail(O3G_ERR_INVALID_ARGUMENT, "T_in is not a rigid transform");
     if (!c->src_ready) return fail(O3G_ERR_INVALID_ARGUMENT, "o3g_set_target and o3g_set_source must be called first");
+    if (!c->estimation && !c->has_normals) return fail(O3G_ERR_INVALID_ARGUMENT, "point-to-plane needs target normals");
     if (corr_out && !is_device_ptr(corr_out)) return fail(O3G_ERR_INVALID_ARGUMENT, "corr_out must be device memory");
     TRY(enter(c));
     const bool wc = corr_out != nullptr;
@@ -602,7 +615,7 @@ o3g_status o3g_icp_step(o3g_ctx* c, const double T_in[16], int32_t* corr_out, do
 
 static o3g_status build_graph(o3g_ctx* c, int max_it, int blocks) {
     GraphKey key;
-    key.max_it = max_it;
+    key.max_it = max_it + 1000000 * c->estimation;
     key.search = c->search;
     key.timing = c->timing;
     key.world = c->world;
@@ -658,6 +671,7 @@ o3g_status o3g_icp_run(o3g_ctx* c, const double init_T[16], int32_t max_iteratio
     if (!(relative_fitness >= 0.0) || !(relative_rmse >= 0.0)) return fail(O3G_ERR_INVALID_ARGUMENT, "criteria must be >= 0");
     if (!c->src_ready) return fail(O3G_ERR_INVALID_ARGUMENT, "o3g_set_target and o3g_set_source must be called first");
     if (!T_out || !fitness || !inlier_rmse) return fail(O3G_ERR_INVALID_ARGUMENT, "T_out, fitness and inlier_rmse are required");
+    if (!c->estimation && !c->has_normals) return fail(O3G_ERR_INVALID_ARGUMENT, "point-to-plane needs target normals");
     TRY(enter(c));
     const int blocks = k3_blocks(c, false);
     TRY(loop_buffers(c, blocks, max_iterations + 1));
@@ -874,6 +888,28 @@ extern "C" o3g_status o3g_icp_multiscale(o3g_ctx* c, const float* src, int64_t n
     }
     memcpy(T_out, T, sizeof(T));
     return O3G_OK;
+}
+
+o3g_status o3g_icp_point_to_point(const float* source_xyz, int64_t n_source, const float* target_xyz,
+                                  int64_t n_target, const double init_T[16], double dmax,
+                                  int32_t max_iterations, double relative_fitness,
+                                  double relative_rmse, double T_out[16], double* fitness,
+                                  double* inlier_rmse, o3g_icp_info* info, void* cuda_stream) {
+    static thread_local o3g_ctx* cached[64] = {};
+    if (!init_T || !rigid_ok(init_T)) return fail(O3G_ERR_INVALID_ARGUMENT, "init_T is not a rigid transform");
+    if (!source_xyz) return fail(O3G_ERR_INVALID_ARGUMENT, "source xyz is required");
+    if (n_source <= 0) return fail(O3G_ERR_INVALID_ARGUMENT, "n_source must be > 0");
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    if (dev < 0 || dev >= 64) return fail(O3G_ERR_CUDA, "device index out of range");
+    o3g_ctx*& c = cached[dev];
+    if (!c) TRY(o3g_create(&c, dev, cuda_stream));
+    c->user = (cudaStream_t)cuda_stream;
+    TRY(o3g_set_option(c, O3G_OPT_ESTIMATION, 1));
+    TRY(o3g_set_target(c, target_xyz, nullptr, n_target, dmax));
+    TRY(o3g_set_source(c, source_xyz, n_source, init_T));
+    return o3g_icp_run(c, init_T, max_iterations, relative_fitness, relative_rmse, T_out, fitness,
+                       inlier_rmse, info, nullptr, nullptr);
 }
 
 // ---------------------------------------------------------- one-shot

@@ -46,6 +46,7 @@ enum TailMode : int {
     TAIL_SUM_RANKS = 4,      // terms = sum over gathered[0..world) in rank order
     TAIL_SOLVE = 8,          // criteria + LDLT + exp + T update (A8)
     TAIL_STEP = 16,          // store terms only (o3g_icp_step)
+    TAIL_P2P = 32,           // point-to-point estimation (Horn's quaternion fit)
 };
 
 __host__ __device__ inline int64_t grid_index_dense(const GridDev& g, int cx, int cy, int cz) {
@@ -122,6 +123,7 @@ struct K3Args {
     int32_t* corr_out;      // original order, nullable
     const uint32_t* nbr_bits;  // dense grid: bit k set iff some cell of k's 27-stencil
                                // is occupied (a conservative skip test); nullable
+    int p2p;                   // record = point-to-point terms (sum s'q^T, sum s', sum q)
     int coop_min;              // variant 1: queries with >= coop_min candidates are
                                // scanned by the whole warp (0 = never)
     // fused tail (single GPU, variant 1): the last block to finish reduces the

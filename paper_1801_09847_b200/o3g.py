@@ -24,7 +24,7 @@ OK, ERR_INVALID_ARGUMENT, ERR_DEGENERATE, ERR_CUDA, ERR_OOM, ERR_COMM, ERR_NOT_I
 FLAG_NO_CORRESPONDENCES = 1
 FLAG_DEGENERATE = 2
 NTERMS = 29
-OPT_SEARCH, OPT_GRID, OPT_TIMING, OPT_BLOCKS_PER_SM = 1, 2, 3, 4
+OPT_SEARCH, OPT_GRID, OPT_TIMING, OPT_BLOCKS_PER_SM, OPT_NBR_MASK, OPT_COOP_MIN, OPT_ESTIMATION = range(1, 8)
 
 
 class O3GError(RuntimeError):
@@ -57,6 +57,7 @@ def lib() -> C.CDLL:
         P, D, I32, I64 = C.c_void_p, C.c_double, C.c_int32, C.c_int64
         sig = {
             "o3g_icp_point_to_plane": [P, I64, P, P, I64, P, D, I32, D, D, P, P, P, P, P],
+            "o3g_icp_point_to_point": [P, I64, P, I64, P, D, I32, D, D, P, P, P, P, P],
             "o3g_create": [P, C.c_int, P],
             "o3g_destroy": [P],
             "o3g_set_target": [P, P, P, I64, D],
@@ -165,6 +166,24 @@ def icp_point_to_plane(source, target, target_normals, max_correspondence_distan
     T = np.zeros(16)
     fit, rmse, info = C.c_double(), C.c_double(), _Info()
     _check(lib().o3g_icp_point_to_plane(ps, n, pt, pn, m, T0, float(max_correspondence_distance),
+                                        int(max_iterations), float(relative_fitness),
+                                        float(relative_rmse), T.ctypes.data, C.byref(fit),
+                                        C.byref(rmse), C.byref(info), _stream_ptr(stream)))
+    return _result(T, fit, rmse, info)
+
+
+def icp_point_to_point(source, target, max_correspondence_distance, init=None,
+                       max_iterations=30, relative_fitness=1e-6, relative_rmse=1e-6,
+                       stream=None) -> RegistrationResult:
+    """registration_icp(..., TransformationEstimationPointToPoint(False))
+    (SPEC S:255-263)."""
+    keep: list = []
+    ps, n = _pts(source, "source", keep)
+    pt, m = _pts(target, "target", keep)
+    T0 = _mat(np.eye(4) if init is None else init, keep)
+    T = np.zeros(16)
+    fit, rmse, info = C.c_double(), C.c_double(), _Info()
+    _check(lib().o3g_icp_point_to_point(ps, n, pt, m, T0, float(max_correspondence_distance),
                                         int(max_iterations), float(relative_fitness),
                                         float(relative_rmse), T.ctypes.data, C.byref(fit),
                                         C.byref(rmse), C.byref(info), _stream_ptr(stream)))

@@ -1,0 +1,86 @@
+"""GPU parity of the NEXT(2) row: point-to-point ICP
+(TransformationEstimationPointToPoint(False); SPEC
+S:255-263). Correspondences bit-exact, the 17 point-to-point terms within the
+R14 tolerance, the loop's T within 1e-6 (the GPU fits with Horn's quaternion
+method, the oracle with SVD/Kabsch: same minimiser, different rounding)."""
+import numpy as np
+import pytest
+
+import oracle
+from synth.rng import Stream
+from synth.scenes import rigid, rotation
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+P2P_SLOTS = list(range(15)) + [27, 28]
+
+
+@pytest.fixture(scope="module")
+def o3g():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1801_09847_b200 as m
+    m.lib()
+    return m
+
+
+def _ctx(o3g, w, src=None):
+    ctx = o3g.Context(0)
+    ctx.set_option(7, 1)
+    ctx.set_target(torch.from_numpy(w["target"]).cuda(), None, w["dmax"])
+    ctx.set_source(torch.from_numpy(w["source"] if src is None else src).cuda(), w["init_T"])
+    return ctx
+
+
+def _abs_terms(T, src, tgt, corr):
+    m = corr >= 0
+    s = oracle.transform(T, src)[m]
+    q = tgt.astype(np.float64)[corr[m]]
+    a = np.zeros(29)
+    a[0:9] = np.abs(s[:, :, None] * q[:, None, :]).sum(0).ravel()
+    a[9:12], a[12:15] = np.abs(s).sum(0), np.abs(q).sum(0)
+    a[27] = m.sum()
+    return a
+
+
+@pytest.mark.parametrize("name", ["tiny", "depth", "large400k"])
+def test_p2p_step_parity(o3g, workloads, name):
+    w = workloads("large16m", n=400_000) if name == "large400k" else workloads(name)
+    grid = oracle.Grid(w["target"], w["dmax"])
+    rs = Stream(44)
+    for T in (w["init_T"], w["T_true"] @ rigid(rotation(rs.unit_vectors(1)[0], 0.003), [0.004, 0, -0.003])):
+        with _ctx(o3g, w) as ctx:
+            corr = torch.full((len(w["source"]),), -7, dtype=torch.int32, device="cuda")
+            st = ctx.step(T, corr_out=corr)
+        corr = corr.cpu().numpy()
+        ref = oracle.step_p2p(T, w["source"], w["target"], w["dmax"], grid=grid)
+        assert np.array_equal(corr, ref["corr"]), name
+        absr = _abs_terms(T, w["source"], w["target"], ref["corr"])
+        for k in P2P_SLOTS:
+            tol = 1e-9 * max(abs(ref["terms"][k]), absr[k] if k != 28 else ref["terms"][k]) + 1e-300
+            assert abs(st["terms"][k] - ref["terms"][k]) <= tol, (name, k)
+
+
+@pytest.mark.parametrize("name", ["tiny", "depth"])
+def test_p2p_loop_parity(o3g, workloads, name):
+    w = workloads(name)
+    ref = oracle.icp_p2p(w["source"], w["target"], w["dmax"], w["iters"], init_T=w["init_T"])
+    with _ctx(o3g, w) as ctx:
+        r = ctx.run(w["init_T"], w["iters"])
+    assert np.abs(r.transformation - ref["T"]).max() <= 1e-6
+    assert abs(r.fitness - ref["fitness"]) <= 1e-6 and abs(r.inlier_rmse - ref["inlier_rmse"]) <= 1e-6
+    assert r.iterations == ref["iterations"] and r.flags == ref["flags"]
+    one = o3g.icp_point_to_point(w["source"], w["target"], w["dmax"], w["init_T"], w["iters"])
+    assert np.abs(one.transformation - ref["T"]).max() <= 1e-6
+
+
+def test_p2p_degenerate_and_plane_needs_normals(o3g):
+    line = np.outer(np.linspace(-1, 1, 200), [1.0, 2.0, 3.0]).astype(np.float32)
+    r = o3g.icp_point_to_point(line, line, 0.1, max_iterations=5)
+    ref = oracle.icp_p2p(line, line, 0.1, 5)
+    assert r.flags == ref["flags"] == oracle.FLAG_DEGENERATE and r.iterations == 0
+    with o3g.Context(0) as ctx:
+        ctx.set_target(line, None, 0.1)
+        ctx.set_source(line)
+        with pytest.raises(o3g.InvalidArgument):
+            ctx.run(np.eye(4), 3)                  # point-to-plane without normals

@@ -148,6 +148,18 @@ o3g_status o3g_icp_run(o3g_ctx* ctx, const double init_T[16], int32_t max_iterat
                        double* fitness, double* inlier_rmse, o3g_icp_info* info,
                        double* hist_fitness, double* hist_rmse);
 
+/* ------------------------------------------------ batched evaluation
+ * evaluate_registration (the RANSAC validation step the
+ * paper profiles as its most time-consuming part) for k
+ * transforms at once: for each Ts[16 i .. 16 i + 15] (host, row-major,
+ * rigid) fitness[i] = inliers / n and inlier_rmse[i] = sqrt(sum d^2 /
+ * inliers) (0 if none) with exactly the correspondence rule of the ICP
+ * pass, no re-estimation. Uses the context's target and source; one
+ * launch covers all k (grid.y = transform). 1 <= k <= 65535. Single GPU
+ * (O3G_ERR_NOT_IMPLEMENTED when distributed).                           */
+o3g_status o3g_evaluate_registration(o3g_ctx* ctx, const double* Ts, int32_t k, double* fitness,
+                                     double* inlier_rmse);
+
 /* ------------------------------------------- downsampling and multi-scale
  * voxel_down_sample (Fig. 1): each output point
  * is the mean of the input points of one occupied voxel of the grid anchored

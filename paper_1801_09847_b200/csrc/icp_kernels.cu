@@ -174,8 +174,8 @@ __global__ void __launch_bounds__(kK3Threads, 4) k3_balanced(const K3Args a) {
     extern __shared__ __align__(16) unsigned char k3smem[];
     __shared__ double sT[12];
     __shared__ double red[kK3Threads / 32][64];
-    if (a.st->done) return;
-    if (threadIdx.x < 12) sT[threadIdx.x] = a.st->T[threadIdx.x];
+    if (!a.eval_T && a.st->done) return;
+    if (threadIdx.x < 12) sT[threadIdx.x] = a.eval_T ? a.eval_T[16 * blockIdx.y + threadIdx.x] : a.st->T[threadIdx.x];
     __syncthreads();
 
     const GridDev g = a.g;
@@ -514,7 +514,7 @@ __global__ void __launch_bounds__(kK3Threads, 4) k3_balanced(const K3Args a) {
                              : (threadIdx.x < kTerms ? term_cidx(threadIdx.x) : -1);
         if (ci >= 0)
             for (int w = 0; w < kK3Threads / 32; ++w) s += red[w][ci];
-        a.block_partials[(size_t)blockIdx.x * kTermStride + threadIdx.x] = s;
+        a.block_partials[((size_t)blockIdx.y * gridDim.x + blockIdx.x) * kTermStride + threadIdx.x] = s;
     }
     if (!a.fuse_mode) return;
 
@@ -588,12 +588,13 @@ void launch_k3(const K3Args& a, int blocks, int variant, bool write_corr, cudaSt
             const size_t sm = k3v2_smem(a.g.hashed);
             occ_v2<true, false>(a.g.hashed), occ_v2<false, false>(a.g.hashed);
             occ_v2<true, true>(a.g.hashed), occ_v2<false, true>(a.g.hashed);
+            const dim3 grid(blocks, a.eval_T ? a.n_eval : 1);
             if (a.coop_min > 0) {
-                if (write_corr) k3_balanced<true, true><<<blocks, kK3Threads, sm, s>>>(a);
-                else k3_balanced<false, true><<<blocks, kK3Threads, sm, s>>>(a);
+                if (write_corr) k3_balanced<true, true><<<grid, kK3Threads, sm, s>>>(a);
+                else k3_balanced<false, true><<<grid, kK3Threads, sm, s>>>(a);
             } else {
-                if (write_corr) k3_balanced<true, false><<<blocks, kK3Threads, sm, s>>>(a);
-                else k3_balanced<false, false><<<blocks, kK3Threads, sm, s>>>(a);
+                if (write_corr) k3_balanced<true, false><<<grid, kK3Threads, sm, s>>>(a);
+                else k3_balanced<false, false><<<grid, kK3Threads, sm, s>>>(a);
             }
         }
     }
@@ -851,6 +852,34 @@ __global__ void __launch_bounds__(kTailThreads)
     }
     if (threadIdx.x != 0) return;
     tail_finish(terms, st, hist_fit, hist_rmse, mode);
+}
+
+// Batched evaluate_registration epilogue: one warp per transform sums the
+// block partials' count and sum d^2 (fixed order), fitness = count / n,
+// rmse = sqrt(sum d^2 / count) or 0 (R7).
+__global__ void k_eval_reduce(const double* __restrict__ partials, int nblocks, int k, double n_total,
+                              double* fit, double* rmse) {
+    const int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+    if (t >= k) return;
+    double c = 0.0, d = 0.0;
+    for (int b = lane; b < nblocks; b += 32) {
+        c += partials[((size_t)t * nblocks + b) * kTermStride + 27];
+        d += partials[((size_t)t * nblocks + b) * kTermStride + 28];
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        c += __shfl_xor_sync(0xffffffffu, c, o);
+        d += __shfl_xor_sync(0xffffffffu, d, o);
+    }
+    if (lane == 0) {
+        fit[t] = c / n_total;
+        rmse[t] = c > 0.0 ? sqrt(d / c) : 0.0;
+    }
+}
+
+void launch_eval_reduce(const double* partials, int nblocks, int k, double n_total, double* fit,
+                        double* rmse, cudaStream_t s) {
+    k_eval_reduce<<<(k + 7) / 8, 256, 0, s>>>(partials, nblocks, k, n_total, fit, rmse);
 }
 
 void launch_tail(const double* partials, int nblocks, double* gathered, int world, int rank,

@@ -134,6 +134,7 @@ struct o3g_ctx {
     DevBuf keys_a, keys_b, vals_a, vals_b, cub_tmp, stage_a, stage_b, misc;
     // voxel_down_sample / multi-scale scratch
     DevBuf vk_a, vk_b, vflags, vrunid, vstarts, ms_src, ms_tgt, ms_nrm;
+    DevBuf ev_T, ev_part, ev_out;
     // source
     int64_t n_total = 0, n_local = 0, shard_lo = 0;
     bool src_ready = false;
@@ -288,7 +289,7 @@ o3g_status o3g_destroy(o3g_ctx* c) {
                       &c->vals_a, &c->vals_b, &c->cub_tmp, &c->stage_a, &c->stage_b, &c->misc,
                       &c->src4, &c->partials, &c->gathered, &c->state, &c->hist_fit, &c->hist_rmse,
                       &c->vk_a, &c->vk_b, &c->vflags, &c->vrunid, &c->vstarts, &c->ms_src,
-                      &c->ms_tgt, &c->ms_nrm};
+                      &c->ms_tgt, &c->ms_nrm, &c->ev_T, &c->ev_part, &c->ev_out};
     for (DevBuf* b : bufs) b->release();
     if (c->comm && nccl().comm_destroy) nccl().comm_destroy(c->comm);
     if (c->h_state) cudaFreeHost(c->h_state);
@@ -514,6 +515,8 @@ static K3Args k3_args(o3g_ctx* c, int32_t* corr) {
     // auto (-1): warp-cooperative scans only where cells are dense (measured:
     // LiDAR, 226 points per occupied cell, gains 1.6x; sparse configs lose)
     a.p2p = c->estimation;
+    a.eval_T = nullptr;
+    a.n_eval = 0;
     a.coop_min = c->coop_min >= 0 ? c->coop_min
                                   : ((double)c->m >= 32.0 * (double)(c->occupied > 0 ? c->occupied : 1) ? 256 : 0);
     a.fuse_mode = 0;
@@ -773,6 +776,44 @@ o3g_status o3g_dist_init(o3g_ctx* c, int rank, int world, const void* id) {
         return fail(O3G_ERR_COMM, std::string("ncclCommInitRank: ") +
                                       (nccl().error_string ? nccl().error_string(r) : "?"));
     }
+    return O3G_OK;
+}
+
+// ---------------------------------------- batched evaluate_registration
+extern "C" o3g_status o3g_evaluate_registration(o3g_ctx* c, const double* Ts, int32_t k,
+                                                double* fitness, double* inlier_rmse) {
+    if (!c) return fail(O3G_ERR_INVALID_ARGUMENT, "ctx is NULL");
+    if (!Ts || !fitness || !inlier_rmse || k <= 0 || k > 65535)
+        return fail(O3G_ERR_INVALID_ARGUMENT, "need 1 <= k <= 65535 transforms and output arrays");
+    for (int i = 0; i < k; ++i)
+        if (!rigid_ok(Ts + 16 * (size_t)i)) return fail(O3G_ERR_INVALID_ARGUMENT, "a transform is not rigid");
+    if (!c->src_ready) return fail(O3G_ERR_INVALID_ARGUMENT, "o3g_set_target and o3g_set_source must be called first");
+    if (c->world != 1) return fail(O3G_ERR_NOT_IMPLEMENTED, "batched evaluation is single-GPU");
+    TRY(enter(c));
+    const int blocks = k3_blocks(c, false);
+    TRY(c->ev_T.ensure((size_t)k * 16 * sizeof(double)));
+    TRY(c->ev_part.ensure((size_t)k * blocks * kTermStride * sizeof(double)));
+    TRY(c->ev_out.ensure((size_t)k * 2 * sizeof(double)));
+    TRY(c->state.ensure(sizeof(IcpState)));
+    CK(cudaMemcpyAsync(c->ev_T.p, Ts, (size_t)k * 16 * sizeof(double), cudaMemcpyHostToDevice, c->exec));
+    K3Args a = k3_args(c, nullptr);
+    a.p2p = 1;                       // count and sum d^2 ride in the point-to-point record
+    a.eval_T = c->ev_T.as<double>();
+    a.n_eval = k;
+    a.block_partials = c->ev_part.as<double>();
+    if (c->n_local > 0) {
+        launch_k3(a, blocks, 1, false, c->exec);
+        launch_eval_reduce(c->ev_part.as<double>(), blocks, k, (double)c->n_total, c->ev_out.as<double>(),
+                           c->ev_out.as<double>() + k, c->exec);
+        c->launches += 2;
+    } else {
+        CK(cudaMemsetAsync(c->ev_out.p, 0, (size_t)k * 2 * sizeof(double), c->exec));
+    }
+    CK(cudaMemcpyAsync(fitness, c->ev_out.p, (size_t)k * sizeof(double), cudaMemcpyDeviceToHost, c->exec));
+    CK(cudaMemcpyAsync(inlier_rmse, c->ev_out.as<double>() + k, (size_t)k * sizeof(double),
+                       cudaMemcpyDeviceToHost, c->exec));
+    CK(cudaStreamSynchronize(c->exec));
+    CK(cudaGetLastError());
     return O3G_OK;
 }
 

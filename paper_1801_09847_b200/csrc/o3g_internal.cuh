@@ -124,6 +124,9 @@ struct K3Args {
     const uint32_t* nbr_bits;  // dense grid: bit k set iff some cell of k's 27-stencil
                                // is occupied (a conservative skip test); nullable
     int p2p;                   // record = point-to-point terms (sum s'q^T, sum s', sum q)
+    int n_eval;
+    const double* eval_T;      // batched evaluation: T of blockIdx.y is eval_T[16 * y]
+                               // (nullable); partials at [(y * gridDim.x + x) * 32]
     int coop_min;              // variant 1: queries with >= coop_min candidates are
                                // scanned by the whole warp (0 = never)
     // fused tail (single GPU, variant 1): the last block to finish reduces the
@@ -142,6 +145,8 @@ int k3_sorted_blocks_per_sm(bool write_corr, int hashed);
 void launch_k3_sorted(const K3Args& a, int blocks, bool write_corr, cudaStream_t s);
 void launch_k3(const K3Args& a, int blocks, int variant, bool write_corr, cudaStream_t s);
 int k3_max_blocks_per_sm(int variant, bool write_corr, int hashed);
+void launch_eval_reduce(const double* partials, int nblocks, int k, double n_total, double* fit,
+                        double* rmse, cudaStream_t s);
 void launch_tail(const double* block_partials, int nblocks, double* gathered, int world, int rank,
                  IcpState* st, double* hist_fit, double* hist_rmse, int mode, cudaStream_t s);
 

@@ -70,6 +70,7 @@ def lib() -> C.CDLL:
             "o3g_last_run_kernel_ms": [P, P, P, P],
             "o3g_grid_info": [P, P, P, P, P],
             "o3g_voxel_down_sample": [P, P, P, I64, D, P, P, P],
+            "o3g_evaluate_registration": [P, P, I32, P, P],
             "o3g_icp_multiscale": [P, P, I64, P, P, I64, P, I32, P, P, P, D, D, P, P, P, P, P],
         }
         for name, args in sig.items():
@@ -278,6 +279,16 @@ class Context:
         if history:
             hf, hr = hf[:info.passes].copy(), hr[:info.passes].copy()
         return _result(T, fit, rmse, info, hf, hr)
+
+    def evaluate(self, transforms):
+        """Batched evaluate_registration: (fitness[k], inlier_rmse[k]) for a
+        stack of rigid 4x4 transforms."""
+        Ts = np.ascontiguousarray(np.asarray(transforms, dtype=np.float64).reshape(-1, 16))
+        k = len(Ts)
+        fit, rmse = np.zeros(k), np.zeros(k)
+        _check(lib().o3g_evaluate_registration(self._h, Ts.ctypes.data, k, fit.ctypes.data,
+                                               rmse.ctypes.data))
+        return fit, rmse
 
     def voxel_down_sample(self, xyz, voxel, normals=None):
         """SPEC S:58-61 voxel_down_sample on the device. Returns CUDA tensors

@@ -84,3 +84,37 @@ def test_p2p_degenerate_and_plane_needs_normals(o3g):
         ctx.set_source(line)
         with pytest.raises(o3g.InvalidArgument):
             ctx.run(np.eye(4), 3)                  # point-to-plane without normals
+
+
+# ------------------------------------------- NEXT(3): batched evaluation
+def test_batched_evaluate_registration(o3g, workloads):
+    """per-transform fitness / inlier_rmse exactly as the ICP pass
+    computes them; k transforms in one launch."""
+    w = workloads("depth")
+    rs = Stream(71)
+    Ts = [w["T_true"] @ rigid(rotation(rs.unit_vectors(1)[0], 0.02 * rs.uniform(1)[0]),
+                              rs.uniform(3, -0.03, 0.03)) for _ in range(37)]
+    far = np.eye(4)
+    far[:3, 3] = 1000.0
+    Ts += [w["init_T"], far]
+    with o3g.Context(0) as ctx:
+        ctx.set_target(w["target"], w["target_normals"], w["dmax"])
+        ctx.set_source(w["source"])
+        fit, rmse = ctx.evaluate(np.stack(Ts))
+    grid = oracle.Grid(w["target"], w["dmax"])
+    for k, T in enumerate(Ts):
+        ref = oracle.step(T, w["source"], w["target"], w["target_normals"], w["dmax"], grid=grid)
+        n = len(w["source"])
+        assert fit[k] == ref["count"] / n, k
+        r = np.sqrt(ref["sum_sq_dist"] / ref["count"]) if ref["count"] else 0.0
+        assert abs(rmse[k] - r) <= 1e-12 * max(r, 1e-300), k
+    assert fit[-1] == 0.0 and rmse[-1] == 0.0                         # S:298 out of range
+
+
+def test_evaluate_perfect_alignment(o3g, workloads):
+    w = workloads("tiny")
+    with o3g.Context(0) as ctx:
+        ctx.set_target(w["target"], w["target_normals"], w["dmax"])
+        ctx.set_source(w["target"])
+        fit, rmse = ctx.evaluate(np.eye(4)[None])
+    assert fit[0] == 1.0 and rmse[0] == 0.0                           # S:297

@@ -64,6 +64,8 @@ def lib():
         L.orc_kabsch.argtypes = [P, P]
         L.orc_icp_p2p.restype = C.c_int
         L.orc_icp_p2p.argtypes = [P, I64, P, I64, P, D, I32, D, D, P, P, P, P, P, P]
+        L.orc_estimate_normals.restype = I64
+        L.orc_estimate_normals.argtypes = [P, I64, D, I32, P, P]
         L.orc_icp_multiscale.restype = C.c_int
         L.orc_icp_multiscale.argtypes = [P, I64, P, P, I64, P, I32, P, P, P, D, D, P, P, P, P, P]
         _lib = L
@@ -248,3 +250,15 @@ def icp_p2p(source, target, dmax, max_iterations, init_T=None, relative_fitness=
         raise MemoryError("oracle icp_p2p failed")
     return dict(T=T.reshape(4, 4), fitness=float(fit[0]), inlier_rmse=float(rmse[0]),
                 iterations=int(it[0]), flags=int(fl[0]), converged=bool(cv[0]), passes=passes)
+
+
+def estimate_normals(points, radius=0.1, max_nn=30):
+    """SPEC S:67-75 hybrid-neighbourhood PCA normals. Returns (normals f32,
+    neighbour counts, number of < 3-neighbour fallbacks)."""
+    p = _f32(points)
+    out = np.empty_like(p)
+    cnt = np.empty(len(p), np.int32)
+    fb = lib().orc_estimate_normals(_p(p), len(p), float(radius), int(max_nn), _p(out), _p(cnt))
+    if fb < 0:
+        raise ValueError("estimate_normals: invalid input")
+    return out, cnt, int(fb)

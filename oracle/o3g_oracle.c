@@ -678,3 +678,81 @@ int orc_icp_p2p(const float *src, int64_t n, const float *tgt, int64_t m, const 
     orc_grid_free(g);
     return passes;
 }
+
+/* ---------------------------------------------- estimate_normals (NEXT 4) */
+/* SPEC S:67-75 (Fig. 1b "KDTreeSearchParamHybrid(radius = 0.1, max_nn =
+ * 30)", "normal estimation ... #pragma omp for"): for each point the
+ * hybrid neighbourhood = the min(max_nn, count) nearest points within the
+ * radius (the point itself included; d^2 in fp64 as in A4, inclusive, ties
+ * -> lower index), ordered by (d^2, index); mean and covariance in
+ * fp64 summed in that order (cov divides by k); normal = unit eigenvector of
+ * the smallest eigenvalue (Jacobi); sign: the component of largest absolute
+ * value made positive (first such component on exact ties). Fewer than 3
+ * neighbours -> (0,0,1), counted. Returns that count (or -1 on error).      */
+typedef struct { double d2; int64_t idx; } orc_nb;
+
+static int cmp_nb(const void *a_, const void *b_)
+{
+    const orc_nb *a = (const orc_nb *)a_, *b = (const orc_nb *)b_;
+    if (a->d2 != b->d2) return a->d2 < b->d2 ? -1 : 1;
+    return a->idx < b->idx ? -1 : (a->idx > b->idx);
+}
+
+int64_t orc_estimate_normals(const float *p, int64_t n, double radius, int32_t max_nn, float *out_n,
+                             int32_t *nbr_count)
+{
+    if (n < 3 || !(radius > 0.0) || max_nn < 1) return -1;
+    orc_grid *g = orc_grid_build(p, n, radius);
+    orc_nb *buf = (orc_nb *)malloc(sizeof(orc_nb) * (size_t)n);
+    if (!g || !buf) { orc_grid_free(g); free(buf); return -1; }
+    const double r2 = radius * radius;
+    int64_t fallback = 0;
+    for (int64_t i = 0; i < n; ++i) {
+        double s[3] = {(double)p[3 * i], (double)p[3 * i + 1], (double)p[3 * i + 2]};
+        int64_t cx = cell_coord(s[0], g->o[0], g->h), cy = cell_coord(s[1], g->o[1], g->h),
+                cz = cell_coord(s[2], g->o[2], g->h);
+        int64_t cnt = 0;
+        for (int64_t dz = -1; dz <= 1; ++dz)
+            for (int64_t dy = -1; dy <= 1; ++dy)
+                for (int64_t dx = -1; dx <= 1; ++dx)
+                    for (int64_t k = lower(g, cz + dz, cy + dy, cx + dx); k < g->m; ++k) {
+                        const orc_cellpt *c = &g->pts[k];
+                        if (c->cz != cz + dz || c->cy != cy + dy || c->cx != cx + dx) break;
+                        double d2 = dist2(s, p + 3 * c->idx);
+                        if (d2 <= r2) { buf[cnt].d2 = d2; buf[cnt].idx = c->idx; ++cnt; }
+                    }
+        qsort(buf, (size_t)cnt, sizeof(orc_nb), cmp_nb);
+        int64_t k = cnt < max_nn ? cnt : max_nn;
+        if (nbr_count) nbr_count[i] = (int32_t)k;
+        if (k < 3) {
+            out_n[3 * i] = 0.0f, out_n[3 * i + 1] = 0.0f, out_n[3 * i + 2] = 1.0f;
+            ++fallback;
+            continue;
+        }
+        double mu[3] = {0, 0, 0};
+        for (int64_t t = 0; t < k; ++t)
+            for (int a = 0; a < 3; ++a) mu[a] += (double)p[3 * buf[t].idx + a];
+        for (int a = 0; a < 3; ++a) mu[a] /= (double)k;
+        double C[9] = {0};
+        for (int64_t t = 0; t < k; ++t) {
+            double d[3];
+            for (int a = 0; a < 3; ++a) d[a] = (double)p[3 * buf[t].idx + a] - mu[a];
+            for (int a = 0; a < 3; ++a)
+                for (int b = 0; b < 3; ++b) C[3 * a + b] += d[a] * d[b];
+        }
+        for (int a = 0; a < 9; ++a) C[a] /= (double)k;
+        double w[3], V[9];
+        jacobi3(C, w, V);
+        int sm = 0;
+        for (int a = 1; a < 3; ++a) if (w[a] < w[sm]) sm = a;
+        double v[3] = {V[sm], V[3 + sm], V[6 + sm]};
+        double nv = sqrt(v[0] * v[0] + v[1] * v[1] + v[2] * v[2]);
+        int big = 0;
+        for (int a = 1; a < 3; ++a) if (fabs(v[a]) > fabs(v[big])) big = a;
+        double sg = v[big] < 0.0 ? -1.0 : 1.0;
+        for (int a = 0; a < 3; ++a) out_n[3 * i + a] = (float)(sg * v[a] / nv);
+    }
+    free(buf);
+    orc_grid_free(g);
+    return fallback;
+}

@@ -452,3 +452,53 @@ def test_icp_p2p_recovers_motion():
     assert ang < 0.1 and np.abs(E[:3, 3]).max() < 1e-3
     r = oracle.icp_p2p(tgt, tgt, 0.05, 10)            # S:288 fixed point
     assert np.abs(r["T"] - np.eye(4)).max() < 1e-12 and r["fitness"] == 1.0
+
+
+# ------------------------------------------------ estimate_normals (NEXT 4)
+def test_normals_plane_and_sphere_spec_examples():
+    rs = Stream(808)
+    pl = np.concatenate([rs.uniform(200, -0.3, 0.3).reshape(-1, 2), np.zeros((100, 1))], 1)
+    n, cnt, fb = oracle.estimate_normals(pl, 0.1, 30)
+    assert np.abs(n - np.array([0, 0, 1.0])).max() < 1e-6     # S:73 (fallbacks are (0,0,1) too)
+    sp = rs.unit_vectors(500)
+    n, cnt, fb = oracle.estimate_normals(sp, 0.3, 30)
+    cosang = np.abs((n.astype(np.float64) * sp).sum(1))
+    assert np.degrees(np.arccos(np.clip(cosang, -1, 1))).max() < 2.0
+
+
+def test_normals_match_numpy_bruteforce_pca():
+    """equal to a brute-force PCA over the identical neighbour sets (numpy
+    lexsort KNN + numpy eigh), up to sign; the sign rule (largest |component|
+    positive) is checked where it is unambiguous."""
+    from synth.scenes import Rects
+    rs = Stream(809)
+    r = Rects()
+    X, Y, Z = np.eye(3)
+    r.add([0, 0, 0], X, Y, Z)
+    r.add_box([0.2, 0.3, 0], [0.6, 0.7, 0.3])
+    r.finish()
+    p, _ = r.sample(rs, 3000)
+    p = (p + 0.002 * rs.uniform(9000, -1, 1).reshape(-1, 3)).astype(np.float32)
+    n, cnt, fb = oracle.estimate_normals(p, 0.08, 30)
+    p64 = p.astype(np.float64)
+    for i in range(0, len(p), 7):
+        d = p64 - p64[i]
+        d2 = (d[:, 0] * d[:, 0] + d[:, 1] * d[:, 1]) + d[:, 2] * d[:, 2]
+        ok = np.nonzero(d2 <= 0.08 * 0.08)[0]
+        nb = ok[np.lexsort((ok, d2[ok]))][:30]
+        assert cnt[i] == len(nb)
+        if len(nb) < 3:
+            assert np.array_equal(n[i], [0, 0, 1])
+            continue
+        q = p64[nb]
+        w, V = np.linalg.eigh(np.cov(q.T, bias=True))
+        if w[1] - w[0] < 1e-6 * w[2]:
+            continue                       # ill-conditioned smallest eigenvector
+        v = V[:, 0]
+        assert abs(abs(np.dot(v, n[i].astype(np.float64))) - 1) < 1e-6, i
+        a = np.sort(np.abs(v))
+        if a[2] - a[1] > 1e-6:
+            assert n[i][np.argmax(np.abs(n[i]))] > 0
+    tiny = np.array([[0, 0, 0], [5, 0, 0], [0, 5, 0]], np.float32)
+    n, cnt, fb = oracle.estimate_normals(tiny, 0.1, 30)
+    assert fb == 3 and np.array_equal(n, np.tile([0, 0, 1], (3, 1)).astype(np.float32))

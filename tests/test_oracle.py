@@ -460,8 +460,10 @@ def test_normals_plane_and_sphere_spec_examples():
     pl = np.concatenate([rs.uniform(200, -0.3, 0.3).reshape(-1, 2), np.zeros((100, 1))], 1)
     n, cnt, fb = oracle.estimate_normals(pl, 0.1, 30)
     assert np.abs(n - np.array([0, 0, 1.0])).max() < 1e-6     # S:73 (fallbacks are (0,0,1) too)
-    sp = rs.unit_vectors(500)
-    n, cnt, fb = oracle.estimate_normals(sp, 0.3, 30)
+    # S:74 gives no search parameters; neighbourhoods of ~50 points keep the
+    # sampling-asymmetry tilt of the PCA normal under 2 degrees
+    sp = rs.unit_vectors(20000)
+    n, cnt, fb = oracle.estimate_normals(sp, 0.1, 100)
     cosang = np.abs((n.astype(np.float64) * sp).sum(1))
     assert np.degrees(np.arccos(np.clip(cosang, -1, 1))).max() < 2.0
 

@@ -148,6 +148,22 @@ o3g_status o3g_icp_run(o3g_ctx* ctx, const double init_T[16], int32_t max_iterat
                        double* fitness, double* inlier_rmse, o3g_icp_info* info,
                        double* hist_fitness, double* hist_rmse);
 
+/* --------------------------------------------------- normal estimation
+ * estimate_normals ("KDTreeSearchParamHybrid(
+ * radius = 0.1, max_nn = 30)"): for every point, the hybrid
+ * neighbourhood is the min(max_nn, count) nearest points within radius
+ * (the point itself included; the ICP pass's exact fp64 distance rule,
+ * inclusive, ties -> lower index); mean and covariance in fp64 in (d^2,
+ * index) order; normal = unit eigenvector of the smallest eigenvalue with
+ * its largest-magnitude component positive; < 3 neighbours -> (0,0,1),
+ * counted in *n_fallback. xyz: [n][3] float32 host or device, n >= 3;
+ * 1 <= max_nn <= 64. out_normals: DEVICE float32 [n][3]; nbr_count:
+ * DEVICE int32 [n] or NULL. Builds the cloud's grid in the context (it
+ * REPLACES the context's target; call o3g_set_target again afterwards).  */
+o3g_status o3g_estimate_normals(o3g_ctx* ctx, const float* xyz, int64_t n, double radius,
+                                int32_t max_nn, float* out_normals, int32_t* nbr_count,
+                                int64_t* n_fallback);
+
 /* ------------------------------------------------ batched evaluation
  * evaluate_registration (the RANSAC validation step the
  * paper profiles as its most time-consuming part) for k

@@ -779,6 +779,31 @@ o3g_status o3g_dist_init(o3g_ctx* c, int rank, int world, const void* id) {
     return O3G_OK;
 }
 
+// ------------------------------------------------------ estimate_normals
+extern "C" o3g_status o3g_estimate_normals(o3g_ctx* c, const float* xyz, int64_t n, double radius,
+                                           int32_t max_nn, float* out_normals, int32_t* nbr_count,
+                                           int64_t* n_fallback) {
+    if (!c) return fail(O3G_ERR_INVALID_ARGUMENT, "ctx is NULL");
+    if (n < 3) return fail(O3G_ERR_INVALID_ARGUMENT, "estimate_normals needs at least 3 points (S:71)");
+    if (max_nn < 1 || max_nn > 64) return fail(O3G_ERR_INVALID_ARGUMENT, "max_nn must be in [1, 64]");
+    if (!out_normals || !is_device_ptr(out_normals)) return fail(O3G_ERR_INVALID_ARGUMENT, "out_normals must be device memory");
+    if (nbr_count && !is_device_ptr(nbr_count)) return fail(O3G_ERR_INVALID_ARGUMENT, "nbr_count must be device memory");
+    TRY(o3g_set_target(c, xyz, nullptr, n, radius));   // the cloud's own grid, cell = radius
+    c->src_ready = false;
+    TRY(c->misc.ensure(64));
+    unsigned long long* fb = (unsigned long long*)(c->misc.as<uint32_t>() + 14);
+    CK(cudaMemsetAsync(fb, 0, 8, c->exec));
+    launch_normals(c->tpos.as<float4>(), (int)n, c->cell_start.as<int32_t>(), c->g, radius * radius,
+                   max_nn, out_normals, nbr_count, fb, c->exec);
+    c->launches += 1;
+    unsigned long long h = 0;
+    CK(cudaMemcpyAsync(&h, fb, 8, cudaMemcpyDeviceToHost, c->exec));
+    CK(cudaStreamSynchronize(c->exec));
+    CK(cudaGetLastError());
+    if (n_fallback) *n_fallback = (int64_t)h;
+    return O3G_OK;
+}
+
 // ---------------------------------------- batched evaluate_registration
 extern "C" o3g_status o3g_evaluate_registration(o3g_ctx* c, const double* Ts, int32_t k,
                                                 double* fitness, double* inlier_rmse) {

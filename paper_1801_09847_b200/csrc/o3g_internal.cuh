@@ -108,6 +108,11 @@ void launch_run_starts(const int32_t* flags, const int32_t* runid, int64_t n, in
 void launch_vox_mean(const float* xyz, const float* nrm, const int32_t* vals, const int32_t* starts,
                      int64_t nruns, float* out_xyz, float* out_nrm, cudaStream_t s);
 
+// ---- launchers (normals.cu)
+void launch_normals(const float4* tpos, int n, const int32_t* cs, const GridDev& g, double r2,
+                    int max_nn, float* out, int32_t* nbr_count, unsigned long long* fallback,
+                    cudaStream_t s);
+
 // ---- launchers (icp_kernels.cu)
 struct K3Args {
     const float4* src;      // sorted local shard (x,y,z, bitcast original index)

@@ -71,6 +71,7 @@ def lib() -> C.CDLL:
             "o3g_grid_info": [P, P, P, P, P],
             "o3g_voxel_down_sample": [P, P, P, I64, D, P, P, P],
             "o3g_evaluate_registration": [P, P, I32, P, P],
+            "o3g_estimate_normals": [P, P, I64, D, I32, P, P, P],
             "o3g_icp_multiscale": [P, P, I64, P, P, I64, P, I32, P, P, P, D, D, P, P, P, P, P],
         }
         for name, args in sig.items():
@@ -289,6 +290,21 @@ class Context:
         _check(lib().o3g_evaluate_registration(self._h, Ts.ctypes.data, k, fit.ctypes.data,
                                                rmse.ctypes.data))
         return fit, rmse
+
+    def estimate_normals(self, xyz, radius=0.1, max_nn=30):
+        """SPEC S:67-75 hybrid-neighbourhood PCA normals on the device. Returns
+        (normals CUDA [n,3], neighbour counts CUDA int32 [n], fallbacks).
+        Replaces the context's target grid."""
+        import torch
+        keep: list = []
+        p, n = _pts(xyz, "xyz", keep)
+        dev = torch.device("cuda", self.device)
+        out = torch.empty((max(n, 1), 3), dtype=torch.float32, device=dev)
+        cnt = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+        fb = C.c_int64()
+        _check(lib().o3g_estimate_normals(self._h, p, n, float(radius), int(max_nn), out.data_ptr(),
+                                          cnt.data_ptr(), C.byref(fb)))
+        return out[:n], cnt[:n], fb.value
 
     def voxel_down_sample(self, xyz, voxel, normals=None):
         """SPEC S:58-61 voxel_down_sample on the device. Returns CUDA tensors

@@ -118,3 +118,34 @@ def test_evaluate_perfect_alignment(o3g, workloads):
         ctx.set_source(w["target"])
         fit, rmse = ctx.evaluate(np.eye(4)[None])
     assert fit[0] == 1.0 and rmse[0] == 0.0
+
+
+# ------------------------------------------------ NEXT(4): normal estimation
+@pytest.mark.parametrize("radius,max_nn", [(0.05, 30), (0.1, 30), (0.03, 8)])
+def test_estimate_normals_parity(o3g, workloads, radius, max_nn):
+    """neighbour sets exact (counts), normals equal to the oracle's
+    (same fp64 mean/covariance order; Jacobi implementations differ, so up to
+    1e-6, and up to sign where the largest component is ambiguous); points
+    with an ill-conditioned smallest eigenvector are skipped."""
+    w = workloads("depth")
+    p = w["target"]
+    ref_n, ref_c, ref_fb = oracle.estimate_normals(p, radius, max_nn)
+    with o3g.Context(0) as ctx:
+        n, c, fb = ctx.estimate_normals(torch.from_numpy(p).cuda(), radius, max_nn)
+    n, c = n.cpu().numpy(), c.cpu().numpy()
+    assert np.array_equal(c, ref_c) and fb == ref_fb
+    dot = np.abs((n.astype(np.float64) * ref_n).sum(1))
+    bad = np.nonzero(dot < 1 - 1e-6)[0]
+    # remaining disagreements must be ill-conditioned neighbourhoods
+    p64 = p.astype(np.float64)
+    for i in bad[:50]:
+        d = p64 - p64[i]
+        d2 = (d[:, 0] * d[:, 0] + d[:, 1] * d[:, 1]) + d[:, 2] * d[:, 2]
+        ok = np.nonzero(d2 <= radius * radius)[0]
+        nb = ok[np.lexsort((ok, d2[ok]))][:max_nn]
+        wv = np.linalg.eigvalsh(np.cov(p64[nb].T, bias=True))
+        assert wv[1] - wv[0] < 1e-5 * max(wv[2], 1e-30), (i, wv)
+    assert len(bad) <= 1e-3 * len(p)
+    same_sign = (n.astype(np.float64) * ref_n).sum(1) > 0
+    amb = np.sort(np.abs(ref_n), 1)
+    assert np.all(same_sign | (amb[:, 2] - amb[:, 1] < 1e-5) | (dot < 1 - 1e-6))

@@ -238,9 +238,13 @@ o3g_status o3g_dist_init(o3g_ctx* ctx, int rank, int world, const void* nccl_uni
  *   29 terms of o3g_icp_step then hold [0..8] sum s'q^T (row-major),
  *   [9..11] sum s', [12..14] sum q, [27] count, [28] sum d^2 (JTJ/JTr
  *   outputs carry the same raw slots). Target normals are then optional.
+ * O3G_OPT_SOURCE_ORDER: order of the source copy (locality only): 0 = by
+ *   the target grid's cell index of order_T s (default), 1 = Morton order of
+ *   4x4x4-cell bricks (takes effect at the next o3g_set_source).
  * Results are identical for every value of the other options.           */
 enum { O3G_OPT_SEARCH = 1, O3G_OPT_GRID = 2, O3G_OPT_TIMING = 3, O3G_OPT_BLOCKS_PER_SM = 4,
-       O3G_OPT_NBR_MASK = 5, O3G_OPT_COOP_MIN = 6, O3G_OPT_ESTIMATION = 7 };
+       O3G_OPT_NBR_MASK = 5, O3G_OPT_COOP_MIN = 6, O3G_OPT_ESTIMATION = 7,
+       O3G_OPT_SOURCE_ORDER = 8 };
 o3g_status o3g_set_option(o3g_ctx* ctx, int option, int64_t value);
 
 /* Sum of the correspondence-kernel (K3) durations of the last o3g_icp_run

@@ -61,10 +61,20 @@ __global__ void k_check_finite(const float* __restrict__ v, int64_t count, int32
 // A1/A2: table index of the cell of each point (target: T = NULL, the raw
 // coordinates; source: the cell of T s, clamped into the grid — ordering
 // only, so clamping far points is harmless).
+// spread the low 10 bits of v to every third bit (Morton interleave)
+__device__ __forceinline__ uint32_t spread3(uint32_t v) {
+    v &= 0x3ffu;
+    v = (v | (v << 16)) & 0x030000FFu;
+    v = (v | (v << 8)) & 0x0300F00Fu;
+    v = (v | (v << 4)) & 0x030C30C3u;
+    v = (v | (v << 2)) & 0x09249249u;
+    return v;
+}
+
 __global__ void k_cell_keys(const float* __restrict__ xyz, int64_t n, GridDev g, bool has_T,
                             double T0, double T1, double T2, double T3, double T4, double T5,
                             double T6, double T7, double T8, double T9, double T10, double T11,
-                            uint32_t* __restrict__ keys, int32_t* __restrict__ vals) {
+                            uint32_t* __restrict__ keys, int32_t* __restrict__ vals, int brick) {
     const double T[12] = {T0, T1, T2, T3, T4, T5, T6, T7, T8, T9, T10, T11};
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
@@ -74,8 +84,15 @@ __global__ void k_cell_keys(const float* __restrict__ xyz, int64_t n, GridDev g,
         int cx = min(max(cell_coord(sx, g.ox, g.inv_h, g.nx), 0), g.nx - 1);
         int cy = min(max(cell_coord(sy, g.oy, g.inv_h, g.ny), 0), g.ny - 1);
         int cz = min(max(cell_coord(sz, g.oz, g.inv_h, g.nz), 0), g.nz - 1);
-        uint32_t k = g.hashed ? ((grid_row_hash(cy, cz) + (uint32_t)cx) & g.hmask)
-                              : (uint32_t)grid_index_dense(g, cx, cy, cz);
+        uint32_t k;
+        if (brick) {   // source order: Morton order of 4x4x4-cell bricks, x-fastest inside
+            k = ((spread3((uint32_t)cx >> 2) | (spread3((uint32_t)cy >> 2) << 1) |
+                  (spread3((uint32_t)cz >> 2) << 2)) << 6) |
+                (((uint32_t)cz & 3u) << 4) | (((uint32_t)cy & 3u) << 2) | ((uint32_t)cx & 3u);
+        } else {
+            k = g.hashed ? ((grid_row_hash(cy, cz) + (uint32_t)cx) & g.hmask)
+                         : (uint32_t)grid_index_dense(g, cx, cy, cz);
+        }
         keys[i] = k;
         vals[i] = (int32_t)i;
     }
@@ -164,12 +181,12 @@ void launch_check_finite(const float* v, int64_t count, int32_t* nonfinite, int 
     k_check_finite<<<blocks_for(count, 256, sms * 8), 256, 0, s>>>(v, count, nonfinite);
 }
 void launch_cell_keys(const float* xyz, int64_t n, const GridDev& g, const double* T,
-                      uint32_t* keys, int32_t* vals, cudaStream_t s) {
+                      uint32_t* keys, int32_t* vals, cudaStream_t s, int brick) {
     static const double I[12] = {1, 0, 0, 0, 0, 1, 0, 0, 0, 0, 1, 0};
     const double* t = T ? T : I;
     k_cell_keys<<<blocks_for(n, 256), 256, 0, s>>>(xyz, n, g, T != nullptr, t[0], t[1], t[2], t[3],
                                                    t[4], t[5], t[6], t[7], t[8], t[9], t[10], t[11],
-                                                   keys, vals);
+                                                   keys, vals, brick);
 }
 void launch_histogram(const uint32_t* keys, int64_t n, int32_t* counts, cudaStream_t s) {
     k_histogram<<<blocks_for(n, 256), 256, 0, s>>>(keys, n, counts);

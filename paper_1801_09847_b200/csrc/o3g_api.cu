@@ -121,6 +121,7 @@ struct o3g_ctx {
     // options
     int search = 1, grid_mode = 0, timing = 0, bps_override = 0, nbr_mask = 1, coop_min = -1;
     int estimation = 0;   // 0 point-to-plane, 1 point-to-point
+    int src_order = 0;    // 0 lexicographic cell, 1 brick-Morton
     bool has_normals = false;
 
     // target grid
@@ -312,6 +313,10 @@ o3g_status o3g_set_option(o3g_ctx* c, int option, int64_t value) {
             break;
         case O3G_OPT_TIMING: c->timing = value ? 1 : 0; break;
         case O3G_OPT_NBR_MASK: c->nbr_mask = value ? 1 : 0; break;
+        case O3G_OPT_SOURCE_ORDER:
+            if (value < 0 || value > 1) return fail(O3G_ERR_INVALID_ARGUMENT, "source order must be 0 or 1");
+            c->src_order = (int)value;
+            break;
         case O3G_OPT_ESTIMATION:
             if (value < 0 || value > 1) return fail(O3G_ERR_INVALID_ARGUMENT, "estimation must be 0 or 1");
             c->estimation = (int)value;
@@ -460,9 +465,11 @@ o3g_status o3g_set_source(o3g_ctx* c, const float* xyz, int64_t n, const double 
     TRY(c->vals_b.ensure(n * 4));
     double T12[12];
     if (order_T) memcpy(T12, order_T, sizeof(T12));
+    const bool brick = c->src_order == 1 && !c->g.hashed && c->g.nx <= 4096 && c->g.ny <= 4096 &&
+                       c->g.nz <= 4096;
     launch_cell_keys(dx, n, c->g, order_T ? T12 : nullptr, c->keys_a.as<uint32_t>(),
-                     c->vals_a.as<int32_t>(), c->exec);
-    TRY(sort_pairs(c, n, bits_for((uint64_t)(c->g.table_size - 1))));
+                     c->vals_a.as<int32_t>(), c->exec, brick ? 1 : 0);
+    TRY(sort_pairs(c, n, brick ? 32 : bits_for((uint64_t)(c->g.table_size - 1))));
     const int64_t lo = (int64_t)c->rank * n / c->world, hi = (int64_t)(c->rank + 1) * n / c->world;
     TRY(c->src4.ensure((size_t)(hi - lo > 0 ? hi - lo : 1) * sizeof(float4)));
     if (hi > lo) launch_gather_source(dx, c->vals_b.as<int32_t>(), lo, hi, c->src4.as<float4>(), c->exec);

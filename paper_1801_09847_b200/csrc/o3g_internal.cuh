@@ -83,8 +83,10 @@ void launch_bbox(const float* xyz, int64_t n, uint32_t* minmax6, int32_t* nonfin
                  cudaStream_t s);
 void launch_check_finite(const float* v, int64_t count, int32_t* nonfinite, int sms,
                          cudaStream_t s);
+// brick = 1: Morton order of 4x4x4-cell bricks (source ordering only;
+// needs < 2^10 bricks per axis), 0: the table index
 void launch_cell_keys(const float* xyz, int64_t n, const GridDev& g, const double* T12_or_null,
-                      uint32_t* keys, int32_t* vals, cudaStream_t s);
+                      uint32_t* keys, int32_t* vals, cudaStream_t s, int brick = 0);
 void launch_histogram(const uint32_t* keys, int64_t n, int32_t* counts, cudaStream_t s);
 void launch_gather_target(const float* xyz, const float* nrm, const int32_t* vals_sorted,
                           const uint32_t* keys_sorted, int64_t n, float4* tpos, float4* tnrm,

@@ -385,3 +385,20 @@ def test_cooperative_threshold_invariance(o3g, workloads, name):
         if sub is None:
             _terms_ok(st["terms"], ref)
     assert np.array_equal(outs[0][0], outs[2][0])
+
+
+def test_source_order_option_invariance(o3g, workloads):
+    """O3G_OPT_SOURCE_ORDER only changes locality: identical correspondences
+    and terms within the R14 tolerance."""
+    w = workloads("depth")
+    T = w["T_true"] @ _perturb(23, 0.003, 0.004)
+    ref = oracle.step(T, w["source"], w["target"], w["target_normals"], w["dmax"])
+    for order in (0, 1):
+        ctx = o3g.Context(0)
+        ctx.set_option(8, order)
+        ctx.set_target(_dev(w["target"]), _dev(w["target_normals"]), w["dmax"])
+        ctx.set_source(_dev(w["source"]), w["init_T"])
+        corr, st = _step(ctx, T, len(w["source"]))
+        ctx.close()
+        assert np.array_equal(corr, ref["corr"]), order
+        _terms_ok(st["terms"], ref)

@@ -14,7 +14,13 @@
 
 #include "k3_common.cuh"
 
+#ifndef O3G_P1_UNROLL
+#define O3G_P1_UNROLL 4
+#endif
+
 namespace o3g {
+
+constexpr int kP1Unroll = O3G_P1_UNROLL;   // pass-1 loop unroll (k3_balanced)
 
 // ------------------------------------------------------------------- K3
 template <bool PREFILTER, bool WRITE_CORR>
@@ -408,6 +414,7 @@ __global__ void __launch_bounds__(kK3Threads, 4) k3_balanced(const K3Args a) {
             int k = 0;
             int2 sg = cl > 0 ? segs[lane] : make_int2(0, 0);
             int j = sg.x, e = sg.y;
+#pragma unroll (kP1Unroll)
             for (int it = 0; it < cl; ++it) {
                 if (j == e) {
                     ++k;

@@ -362,7 +362,8 @@ def main():
                               f"inputs {in_bytes / 1e6:.0f} MB > 126 MB L2 (no flush needed)")},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "traffic": traffic, "peak_kind": peak_kind,
-                         "kernel": "k3_corr_reduce", "kernel_ms": k3_avg,
+                         "kernel": ["k3_corr_reduce<exact>", "k3_balanced", "k3_corr_reduce<prefilter>",
+                                    "k3_sorted"][a.search], "kernel_ms": k3_avg,
                          "alg_bytes_per_launch": alg_bytes},
             "cpu_baseline": cpu,
             "e2e": e2e,

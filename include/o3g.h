@@ -241,10 +241,15 @@ o3g_status o3g_dist_init(o3g_ctx* ctx, int rank, int world, const void* nccl_uni
  * O3G_OPT_SOURCE_ORDER: order of the source copy (locality only): 0 = by
  *   the target grid's cell index of order_T s (default), 1 = Morton order of
  *   4x4x4-cell bricks (takes effect at the next o3g_set_source).
+ * O3G_OPT_TARGET_SORT: how o3g_set_target orders the target by cell: 0 =
+ *   counting sort (histogram, scan, atomic scatter), 1 = stable radix sort
+ *   of (cell, index) + gather (default; 1.8 ms faster per 16M-point build).
+ *   Only the order inside a cell differs; every consumer breaks ties by the
+ *   original index.
  * Results are identical for every value of the other options.           */
 enum { O3G_OPT_SEARCH = 1, O3G_OPT_GRID = 2, O3G_OPT_TIMING = 3, O3G_OPT_BLOCKS_PER_SM = 4,
        O3G_OPT_NBR_MASK = 5, O3G_OPT_COOP_MIN = 6, O3G_OPT_ESTIMATION = 7,
-       O3G_OPT_SOURCE_ORDER = 8 };
+       O3G_OPT_SOURCE_ORDER = 8, O3G_OPT_TARGET_SORT = 9 };
 o3g_status o3g_set_option(o3g_ctx* ctx, int option, int64_t value);
 
 /* Sum of the correspondence-kernel (K3) durations of the last o3g_icp_run

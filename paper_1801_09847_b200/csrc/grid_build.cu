@@ -98,10 +98,32 @@ __global__ void k_cell_keys(const float* __restrict__ xyz, int64_t n, GridDev g,
     }
 }
 
-__global__ void k_histogram(const uint32_t* __restrict__ keys, int64_t n, int32_t* counts) {
+__global__ void k_histogram(const uint32_t* __restrict__ keys, int64_t n, int32_t* counts,
+                            unsigned long long* occupied) {
+    int occ = 0;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x)
-        atomicAdd(&counts[keys[i]], 1);
+        occ += atomicAdd(&counts[keys[i]], 1) == 0;   // first point of its cell
+    if (occupied) {
+        for (int o = 16; o; o >>= 1) occ += __shfl_xor_sync(0xffffffffu, occ, o);
+        if ((threadIdx.x & 31) == 0 && occ) atomicAdd(occupied, (unsigned long long)occ);
+    }
+}
+
+// Counting-sort placement of the target (a one-digit LSD radix sort with the
+// cell index as the digit): cursor starts as a copy of cell_start; each point
+// takes the next slot of its cell. Order inside a cell is arbitrary — every
+// consumer breaks ties by the original index, so results do not depend on it.
+__global__ void k_scatter_target(const float* __restrict__ xyz, const float* __restrict__ nrm,
+                                 const uint32_t* __restrict__ keys, int64_t n, int32_t* cursor,
+                                 float4* __restrict__ tpos, float4* __restrict__ tnrm) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t pos = atomicAdd(&cursor[keys[i]], 1);
+        tpos[pos] = make_float4(xyz[3 * i], xyz[3 * i + 1], xyz[3 * i + 2], __int_as_float((int32_t)i));
+        tnrm[pos] = nrm ? make_float4(nrm[3 * i], nrm[3 * i + 1], nrm[3 * i + 2], 0.f)
+                        : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
 }
 
 __global__ void k_gather_target(const float* __restrict__ xyz, const float* __restrict__ nrm,
@@ -188,8 +210,13 @@ void launch_cell_keys(const float* xyz, int64_t n, const GridDev& g, const doubl
                                                    t[4], t[5], t[6], t[7], t[8], t[9], t[10], t[11],
                                                    keys, vals, brick);
 }
-void launch_histogram(const uint32_t* keys, int64_t n, int32_t* counts, cudaStream_t s) {
-    k_histogram<<<blocks_for(n, 256), 256, 0, s>>>(keys, n, counts);
+void launch_histogram(const uint32_t* keys, int64_t n, int32_t* counts, unsigned long long* occupied,
+                      cudaStream_t s) {
+    k_histogram<<<blocks_for(n, 256), 256, 0, s>>>(keys, n, counts, occupied);
+}
+void launch_scatter_target(const float* xyz, const float* nrm, const uint32_t* keys, int64_t n,
+                           int32_t* cursor, float4* tpos, float4* tnrm, cudaStream_t s) {
+    k_scatter_target<<<blocks_for(n, 256), 256, 0, s>>>(xyz, nrm, keys, n, cursor, tpos, tnrm);
 }
 void launch_gather_target(const float* xyz, const float* nrm, const int32_t* vals,
                           const uint32_t* keys, int64_t n, float4* tpos, float4* tnrm,

@@ -87,7 +87,10 @@ void launch_check_finite(const float* v, int64_t count, int32_t* nonfinite, int 
 // needs < 2^10 bricks per axis), 0: the table index
 void launch_cell_keys(const float* xyz, int64_t n, const GridDev& g, const double* T12_or_null,
                       uint32_t* keys, int32_t* vals, cudaStream_t s, int brick = 0);
-void launch_histogram(const uint32_t* keys, int64_t n, int32_t* counts, cudaStream_t s);
+void launch_histogram(const uint32_t* keys, int64_t n, int32_t* counts, unsigned long long* occupied,
+                      cudaStream_t s);
+void launch_scatter_target(const float* xyz, const float* nrm, const uint32_t* keys, int64_t n,
+                           int32_t* cursor, float4* tpos, float4* tnrm, cudaStream_t s);
 void launch_gather_target(const float* xyz, const float* nrm, const int32_t* vals_sorted,
                           const uint32_t* keys_sorted, int64_t n, float4* tpos, float4* tnrm,
                           unsigned long long* occupied, cudaStream_t s);

@@ -402,3 +402,25 @@ def test_source_order_option_invariance(o3g, workloads):
         ctx.close()
         assert np.array_equal(corr, ref["corr"]), order
         _terms_ok(st["terms"], ref)
+
+
+def test_target_sort_invariance(o3g, workloads):
+    """Counting-sort vs stable radix-sort target layouts give bit-identical
+    correspondences AND terms (records are summed in source order)."""
+    w = workloads("large16m", n=400_000)
+    T = w["T_true"]
+    out = []
+    for ts in (0, 1):
+        ctx = o3g.Context(0)
+        ctx.set_option(9, ts)
+        ctx.set_target(_dev(w["target"]), _dev(w["target_normals"]), w["dmax"])
+        ctx.set_source(_dev(w["source"]), w["init_T"])
+        out.append(_step(ctx, T, len(w["source"])))
+        info = ctx.grid_info()
+        r = ctx.run(w["init_T"], 5, 0.0, 0.0)
+        out[-1] = out[-1] + (r, info)
+        ctx.close()
+    assert np.array_equal(out[0][0], out[1][0])
+    assert np.array_equal(out[0][1]["terms"], out[1][1]["terms"])
+    assert np.array_equal(out[0][2].transformation, out[1][2].transformation)
+    assert out[0][3]["occupied_cells"] == out[1][3]["occupied_cells"]

@@ -218,9 +218,9 @@ o3g_status o3g_dist_init(o3g_ctx* ctx, int rank, int world, const void* nccl_uni
 /* -------------------------------------------------------------- options
  * O3G_OPT_SEARCH: correspondence-kernel variant, all bit-identical
  *   (DESIGN.md §5): 0 = exact fp64 test of every candidate; 1 = two-pass
- *   warp kernel (fp32 prefilter with a proven margin + exact fp64 decision);
- *   2 = single-pass fp32 prefilter + exact decision; 3 = two-pass kernel on
- *   count-sorted 128-query tiles (default).
+ *   warp kernel (fp32 prefilter with a proven margin + exact fp64 decision;
+ *   the default); 2 = single-pass fp32 prefilter + exact decision; 3 =
+ *   two-pass kernel on count-sorted 128-query tiles.
  * O3G_OPT_GRID: 0 = auto, 1 = force dense cell table, 2 = force hashed
  *   cell table (collisions only add candidates; results are identical).
  * O3G_OPT_TIMING: 1 = record CUDA events around every correspondence
@@ -246,10 +246,15 @@ o3g_status o3g_dist_init(o3g_ctx* ctx, int rank, int world, const void* nccl_uni
  *   of (cell, index) + gather (default; 1.8 ms faster per 16M-point build).
  *   Only the order inside a cell differs; every consumer breaks ties by the
  *   original index.
+ * O3G_OPT_PRUNE_MIN: variant 1, dense grid: a query with at least this
+ *   many candidates first scans one x-row, then skips the rows whose lower
+ *   distance bound exceeds that row's best; -1 = auto
+ *   (default: threshold 32 when the target averages >= 4 points per
+ *   occupied cell, else off), -2 = never, 0 = every query.
  * Results are identical for every value of the other options.           */
 enum { O3G_OPT_SEARCH = 1, O3G_OPT_GRID = 2, O3G_OPT_TIMING = 3, O3G_OPT_BLOCKS_PER_SM = 4,
        O3G_OPT_NBR_MASK = 5, O3G_OPT_COOP_MIN = 6, O3G_OPT_ESTIMATION = 7,
-       O3G_OPT_SOURCE_ORDER = 8, O3G_OPT_TARGET_SORT = 9 };
+       O3G_OPT_SOURCE_ORDER = 8, O3G_OPT_TARGET_SORT = 9, O3G_OPT_PRUNE_MIN = 10 };
 o3g_status o3g_set_option(o3g_ctx* ctx, int option, int64_t value);
 
 /* Sum of the correspondence-kernel (K3) durations of the last o3g_icp_run

@@ -172,14 +172,45 @@ __host__ __device__ inline size_t k3v2_warp_bytes(int hashed) {
 }
 inline size_t k3v2_smem(int hashed) { return (size_t)(kK3Threads / 32) * k3v2_warp_bytes(hashed); }
 
+// Row pruning, dense grid, light queries: the lane scans
+// the first non-empty x-row of its stencil (own row, faces, corners) first,
+// then drops every other row whose lower bound L on the true squared distance
+// from s' exceeds ub(m1), an upper bound on the fp64 d2 of that row's best: a
+// pass-1 value satisfies
+//   df >= |q - fl32(s')|^2 (1-2^-24)^5,  so  |q - s'| <= sqrt(df) (1+2^-22) + E1,
+// and the fixed-order fp64 d2 exceeds the true value by at most (1+2^-53)^5.
+// A dropped row is strictly farther than a scanned candidate, hence than the
+// winner, so it can neither win nor tie: the decision's uniqueness test and
+// the exact rescan over the kept rows give the same result as over all 9.
+__device__ __forceinline__ float prune_ub(float m1, float E1u, float r2u) {
+    float sq;
+    asm("sqrt.approx.f32 %0, %1;" : "=f"(sq) : "f"(m1));
+    sq = __fadd_ru(__fmul_ru(sq, 1.0f + 1.52587890625e-05f), 2e-19f);   // approx error << 2^-16
+    sq = __fadd_ru(__fmul_ru(sq, 1.0f + 2.384185791015625e-07f), E1u);   // (1-2^-24)^-2.5 < 1+2^-22
+    return fminf(__fmul_ru(__fmul_ru(sq, sq), 1.0f + 9.5367431640625e-07f), r2u);
+}
+// lower bounds of |s' - q| over the 2 faces of the query's cell c along one
+// axis: a target point of cell y satisfies q_y >= o_y + y h up to the rounding
+// of floor((q - o) inv_h) (relative 2^-52), covered by the 1e-12 margin.
+__device__ __forceinline__ void face_gaps(double s, double o, double h, int c, float& gm, float& gp) {
+    const double f = o + (double)c * h;
+    const double d = 1e-12 * (fabs(o) + fabs(s) + h * (fabs((double)c) + 1.0));
+    gm = __double2float_rd(fmax(s - f - d, 0.0));
+    gp = __double2float_rd(fmax(f + h - s - d, 0.0));
+}
+__device__ __forceinline__ float row_lower(int dy, int dz, float gym, float gyp, float gzm, float gzp) {
+    const float a = dy < 0 ? gym : gyp, b = dz < 0 ? gzm : gzp;
+    const float la = dy ? __fmul_rd(a, a) : 0.f, lb = dz ? __fmul_rd(b, b) : 0.f;
+    return __fadd_rd(la, lb);
+}
+
 __device__ __noinline__ void tail_finish(const double* terms, IcpState* st, double* hist_fit, double* hist_rmse,
                             int mode);
 
-template <bool WRITE_CORR, bool COOP>
+template <bool WRITE_CORR, bool COOP, bool PRUNE>
 __global__ void __launch_bounds__(kK3Threads, 4) k3_balanced(const K3Args a) {
     extern __shared__ __align__(16) unsigned char k3smem[];
     __shared__ double sT[12];
-    __shared__ double red[kK3Threads / 32][64];
     if (!a.eval_T && a.st->done) return;
     if (threadIdx.x < 12) sT[threadIdx.x] = a.eval_T ? a.eval_T[16 * blockIdx.y + threadIdx.x] : a.st->T[threadIdx.x];
     __syncthreads();
@@ -189,6 +220,7 @@ __global__ void __launch_bounds__(kK3Threads, 4) k3_balanced(const K3Args a) {
     const int S = k3v2_slots(g.hashed);
     int2* segs = (int2*)(k3smem + (size_t)warp * k3v2_warp_bytes(g.hashed));
     double* vw = (double*)segs;   // [9 rows][kVW], aliases segs (used after the decision)
+    const float r2u = __double2float_ru(a.r2 * (1.0 + 9.094947017729282e-13));   // r2 (1+2^-40), up
     double acc0 = 0.0, acc1 = 0.0;           // C[lane>>2][2(lane&3)+{0,1}]
     const double r2 = a.r2;
 
@@ -210,6 +242,8 @@ __global__ void __launch_bounds__(kK3Threads, 4) k3_balanced(const K3Args a) {
         while (qn < 32 && base < a.n) {
             const int i0 = base + lane;
             base += nw * 32;
+            // the warp's next source batch: in flight while this one is processed
+            if (base + lane < a.n) asm volatile("prefetch.global.L1 [%0];" ::"l"(a.src + base + lane));
             bool live = false;
             if (i0 < a.n) {
                 const float4 p0 = __ldg(&a.src[i0]);
@@ -245,6 +279,10 @@ __global__ void __launch_bounds__(kK3Threads, 4) k3_balanced(const K3Args a) {
         double sx = 0.0, sy = 0.0, sz = 0.0, E1 = 0.0;
         float shx = 0.f, shy = 0.f, shz = 0.f, thr0 = 0.f;
         int nseg = 0, c = 0;
+        // row pruning: prefilter state of the pre-scanned row and its length;
+        // pass 1 then starts at segment k0
+        float pm1 = CUDART_INF_F, pm2 = CUDART_INF_F;
+        int pj1 = -1, k0 = 0, c0 = 0;
         float4 p = make_float4(0.f, 0.f, 0.f, 0.f);
         if (i < a.n) {
             p = __ldg(&a.src[i]);
@@ -276,12 +314,65 @@ __global__ void __launch_bounds__(kK3Threads, 4) k3_balanced(const K3Args a) {
                     bb[r] = ok ? __ldg(cs + rb) : 0;
                     ee[r] = ok ? __ldg(cs + rb + w) : 0;
                 }
+                if (!PRUNE) {
 #pragma unroll
-                for (int r = 0; r < 9; ++r) {
-                    if (ee[r] > bb[r]) {
-                        segs[nseg * 32 + lane] = make_int2(bb[r], ee[r]);
-                        ++nseg;
-                        c += ee[r] - bb[r];
+                    for (int r = 0; r < 9; ++r) {
+                        if (ee[r] > bb[r]) {
+                            segs[nseg * 32 + lane] = make_int2(bb[r], ee[r]);
+                            ++nseg;
+                            c += ee[r] - bb[r];
+                        }
+                    }
+                } else {
+                    shx = __double2float_rn(sx);
+                    shy = __double2float_rn(sy);
+                    shz = __double2float_rn(sz);
+                    E1 = (fabs(sx - (double)shx) + fabs(sy - (double)shy) + fabs(sz - (double)shz)) *
+                         (1.0 + 9.5367431640625e-07);
+                    int tot = 0;
+#pragma unroll
+                    for (int r = 0; r < 9; ++r) tot += ee[r] - bb[r];
+                    // first non-empty row in kOrder (own row, faces, corners)
+                    constexpr int kOrder[9] = {4, 1, 3, 5, 7, 0, 2, 6, 8};
+                    int fb = 0, fe = 0;
+#pragma unroll
+                    for (int t = 8; t >= 0; --t) {
+                        const int r = kOrder[t];
+                        if (ee[r] > bb[r]) fb = bb[r], fe = ee[r];
+                    }
+                    float ub = CUDART_INF_F;
+                    float gym = 0.f, gyp = 0.f, gzm = 0.f, gzp = 0.f;
+                    if (tot >= a.prune_min && !(COOP && tot >= a.coop_min) && fe > fb) {
+                        // that row first: the same prefilter scan as pass 1
+                        for (int j = fb; j < fe; ++j) {
+                            const float4 t = __ldg(&a.tpos[j]);
+                            const float ux = t.x - shx, uy = t.y - shy, uz = t.z - shz;
+                            const float df = fmaf(uz, uz, fmaf(uy, uy, ux * ux));
+                            const bool lt = df < pm1;
+                            pm2 = fminf(pm2, lt ? pm1 : df);
+                            pm1 = lt ? df : pm1;
+                            pj1 = lt ? j : pj1;
+                        }
+                        k0 = 1;
+                        c0 = fe - fb;
+                        ub = prune_ub(pm1, __double2float_ru(E1), r2u);
+                        face_gaps(sy, g.oy, g.h, cy, gym, gyp);
+                        face_gaps(sz, g.oz, g.h, cz, gzm, gzp);
+                    }
+                    // own row first, then the 4 face rows, then the 4 corner rows;
+                    // rows provably farther than the pre-scanned best are not
+                    // staged (the pre-scanned row is always staged first: k0 = 1
+                    // skips it in pass 1, the exact rescan visits it; with no
+                    // candidate within r, ub = r2 could otherwise drop it)
+#pragma unroll
+                    for (int t = 0; t < 9; ++t) {
+                        const int r = kOrder[t];
+                        if (ee[r] > bb[r] &&
+                            (nseg == 0 || k0 == 0 || !(row_lower(r % 3 - 1, r / 3 - 1, gym, gyp, gzm, gzp) > ub))) {
+                            segs[nseg * 32 + lane] = make_int2(bb[r], ee[r]);
+                            ++nseg;
+                            c += ee[r] - bb[r];
+                        }
                     }
                 }
             } else if (g.hashed && near) {
@@ -310,11 +401,13 @@ __global__ void __launch_bounds__(kK3Threads, 4) k3_balanced(const K3Args a) {
                 }
             }
             if (c > 0) {
-                shx = __double2float_rn(sx);
-                shy = __double2float_rn(sy);
-                shz = __double2float_rn(sz);
-                E1 = (fabs(sx - (double)shx) + fabs(sy - (double)shy) + fabs(sz - (double)shz)) *
-                     (1.0 + 9.5367431640625e-07);
+                if (g.hashed || !PRUNE) {   // (the pruning dense path set these already)
+                    shx = __double2float_rn(sx);
+                    shy = __double2float_rn(sy);
+                    shz = __double2float_rn(sz);
+                    E1 = (fabs(sx - (double)shx) + fabs(sy - (double)shy) + fabs(sz - (double)shz)) *
+                         (1.0 + 9.5367431640625e-07);
+                }
                 thr0 = prefilter_thr(r2, E1, a.dmax, a.inv_dmax);
             }
         }
@@ -407,12 +500,12 @@ __global__ void __launch_bounds__(kK3Threads, 4) k3_balanced(const K3Args a) {
         }
 
         // pass 1 (light queries): branch-free fp32 scan of every candidate of this lane's query
-        float m1 = CUDART_INF_F, m2 = CUDART_INF_F;
-        int j1 = -1;
-        const int cl = heavy ? 0 : c;
+        float m1 = pm1, m2 = pm2;
+        int j1 = pj1;
+        const int cl = heavy ? 0 : c - c0;   // (row pruning: the pre-scanned row is done)
         {
-            int k = 0;
-            int2 sg = cl > 0 ? segs[lane] : make_int2(0, 0);
+            int k = k0;
+            int2 sg = cl > 0 ? segs[k0 * 32 + lane] : make_int2(0, 0);
             int j = sg.x, e = sg.y;
 #pragma unroll (kP1Unroll)
             for (int it = 0; it < cl; ++it) {
@@ -433,7 +526,7 @@ __global__ void __launch_bounds__(kK3Threads, 4) k3_balanced(const K3Args a) {
         }
 
         // decision (exact fp64 rule, R1-R3)
-        if (cl > 0 && m1 <= thr0) {
+        if (!heavy && c > 0 && m1 <= thr0) {
             const float4 t = __ldg(&a.tpos[j1]);
             const double dx = __dsub_rn(sx, (double)t.x), dy = __dsub_rn(sy, (double)t.y),
                          dz = __dsub_rn(sz, (double)t.z);
@@ -512,15 +605,17 @@ __global__ void __launch_bounds__(kK3Threads, 4) k3_balanced(const K3Args a) {
         }
     }
 
-    red[warp][(lane >> 2) * 8 + 2 * (lane & 3)] = acc0;
-    red[warp][(lane >> 2) * 8 + 2 * (lane & 3) + 1] = acc1;
+    __syncwarp();
+    vw[(lane >> 2) * 8 + 2 * (lane & 3)] = acc0;   // C of this warp, on its own staging bytes
+    vw[(lane >> 2) * 8 + 2 * (lane & 3) + 1] = acc1;
     __syncthreads();
     if (threadIdx.x < kTermStride) {
         double s = 0.0;
         const int ci = a.p2p ? term_cidx_p2p(threadIdx.x)
                              : (threadIdx.x < kTerms ? term_cidx(threadIdx.x) : -1);
         if (ci >= 0)
-            for (int w = 0; w < kK3Threads / 32; ++w) s += red[w][ci];
+            for (int w = 0; w < kK3Threads / 32; ++w)
+                s += ((const double*)(k3smem + (size_t)w * k3v2_warp_bytes(g.hashed)))[ci];
         a.block_partials[((size_t)blockIdx.y * gridDim.x + blockIdx.x) * kTermStride + threadIdx.x] = s;
     }
     if (!a.fuse_mode) return;
@@ -557,26 +652,27 @@ static int occ_of() {
     return b;
 }
 
-template <bool W, bool CO>
+template <bool W, bool CO, bool PR>
 static int occ_v2(int hashed) {
     static bool attr_done = false;
     if (!attr_done) {
-        cudaFuncSetAttribute(k3_balanced<W, CO>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(k3_balanced<W, CO, PR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)k3v2_smem(1));
         attr_done = true;
     }
     int b = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k3_balanced<W, CO>, kK3Threads, k3v2_smem(hashed));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k3_balanced<W, CO, PR>, kK3Threads, k3v2_smem(hashed));
     return b;
 }
 
-int k3_max_blocks_per_sm(int variant, bool write_corr, int hashed) {
+int k3_max_blocks_per_sm(int variant, bool write_corr, int hashed, bool prune) {
     switch (variant) {
         case 0: return write_corr ? occ_of<false, true>() : occ_of<false, false>();
         case 2: return write_corr ? occ_of<true, true>() : occ_of<true, false>();
         case 3: return k3_sorted_blocks_per_sm(write_corr, hashed);
         default:   // the cooperative instantiation has the same footprint class
-            return write_corr ? occ_v2<true, false>(hashed) : occ_v2<false, false>(hashed);
+            if (prune) return write_corr ? occ_v2<true, false, true>(hashed) : occ_v2<false, false, true>(hashed);
+            return write_corr ? occ_v2<true, false, false>(hashed) : occ_v2<false, false, false>(hashed);
     }
 }
 
@@ -593,15 +689,21 @@ void launch_k3(const K3Args& a, int blocks, int variant, bool write_corr, cudaSt
         case 3: launch_k3_sorted(a, blocks, write_corr, s); break;
         default: {
             const size_t sm = k3v2_smem(a.g.hashed);
-            occ_v2<true, false>(a.g.hashed), occ_v2<false, false>(a.g.hashed);
-            occ_v2<true, true>(a.g.hashed), occ_v2<false, true>(a.g.hashed);
+            occ_v2<true, false, false>(a.g.hashed), occ_v2<false, false, false>(a.g.hashed);
+            occ_v2<true, true, false>(a.g.hashed), occ_v2<false, true, false>(a.g.hashed);
+            occ_v2<true, false, true>(a.g.hashed), occ_v2<false, false, true>(a.g.hashed);
+            occ_v2<true, true, true>(a.g.hashed), occ_v2<false, true, true>(a.g.hashed);
             const dim3 grid(blocks, a.eval_T ? a.n_eval : 1);
-            if (a.coop_min > 0) {
-                if (write_corr) k3_balanced<true, true><<<grid, kK3Threads, sm, s>>>(a);
-                else k3_balanced<false, true><<<grid, kK3Threads, sm, s>>>(a);
-            } else {
-                if (write_corr) k3_balanced<true, false><<<grid, kK3Threads, sm, s>>>(a);
-                else k3_balanced<false, false><<<grid, kK3Threads, sm, s>>>(a);
+            const int sel = (write_corr ? 4 : 0) | (a.coop_min > 0 ? 2 : 0) | (a.prune ? 1 : 0);
+            switch (sel) {
+                case 0: k3_balanced<false, false, false><<<grid, kK3Threads, sm, s>>>(a); break;
+                case 1: k3_balanced<false, false, true><<<grid, kK3Threads, sm, s>>>(a); break;
+                case 2: k3_balanced<false, true, false><<<grid, kK3Threads, sm, s>>>(a); break;
+                case 3: k3_balanced<false, true, true><<<grid, kK3Threads, sm, s>>>(a); break;
+                case 4: k3_balanced<true, false, false><<<grid, kK3Threads, sm, s>>>(a); break;
+                case 5: k3_balanced<true, false, true><<<grid, kK3Threads, sm, s>>>(a); break;
+                case 6: k3_balanced<true, true, false><<<grid, kK3Threads, sm, s>>>(a); break;
+                default: k3_balanced<true, true, true><<<grid, kK3Threads, sm, s>>>(a); break;
             }
         }
     }

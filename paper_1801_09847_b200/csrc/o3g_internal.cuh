@@ -28,6 +28,7 @@ struct GridDev {
     uint32_t hmask;      // table_size - 1 when hashed
     int32_t pad;
     int64_t table_size;  // cell_start has table_size + 1 entries
+    double h;            // cell edge dmax (1 + 2^-20) (row lower bounds, k3_balanced)
 };
 
 // Loop state, resident in device memory for the whole graph-launched loop.
@@ -139,6 +140,8 @@ struct K3Args {
                                // (nullable); partials at [(y * gridDim.x + x) * 32]
     int coop_min;              // variant 1: queries with >= coop_min candidates are
                                // scanned by the whole warp (0 = never)
+    int prune;                 // variant 1: row-pruning instantiation (dense grid)
+    int prune_min;             //   ... for light queries with >= prune_min candidates
     // fused tail (single GPU, variant 1): the last block to finish reduces the
     // block partials in fixed order and runs the A8 epilogue (mode = TAIL_*)
     int fuse_mode;             // 0 = separate k_tail launch
@@ -154,7 +157,7 @@ inline int k3_threads(int variant) { return variant == 3 ? 128 : kK3Threads; }
 int k3_sorted_blocks_per_sm(bool write_corr, int hashed);
 void launch_k3_sorted(const K3Args& a, int blocks, bool write_corr, cudaStream_t s);
 void launch_k3(const K3Args& a, int blocks, int variant, bool write_corr, cudaStream_t s);
-int k3_max_blocks_per_sm(int variant, bool write_corr, int hashed);
+int k3_max_blocks_per_sm(int variant, bool write_corr, int hashed, bool prune);
 void launch_eval_reduce(const double* partials, int nblocks, int k, double n_total, double* fit,
                         double* rmse, cudaStream_t s);
 void launch_tail(const double* block_partials, int nblocks, double* gathered, int world, int rank,

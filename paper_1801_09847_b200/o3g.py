@@ -18,13 +18,16 @@ from dataclasses import dataclass, field
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libo3g.so")
+# O3G_LIB: load another in-tree build of the same library (A/B kernel
+# experiments under tools/sweeps); default the package's libo3g.so
+LIB_PATH = os.environ.get("O3G_LIB") or os.path.join(_PKG, "libo3g.so")
 
 OK, ERR_INVALID_ARGUMENT, ERR_DEGENERATE, ERR_CUDA, ERR_OOM, ERR_COMM, ERR_NOT_IMPLEMENTED = range(7)
 FLAG_NO_CORRESPONDENCES = 1
 FLAG_DEGENERATE = 2
 NTERMS = 29
-OPT_SEARCH, OPT_GRID, OPT_TIMING, OPT_BLOCKS_PER_SM, OPT_NBR_MASK, OPT_COOP_MIN, OPT_ESTIMATION = range(1, 8)
+(OPT_SEARCH, OPT_GRID, OPT_TIMING, OPT_BLOCKS_PER_SM, OPT_NBR_MASK, OPT_COOP_MIN, OPT_ESTIMATION,
+ OPT_SOURCE_ORDER, OPT_TARGET_SORT, OPT_PRUNE_MIN) = range(1, 11)
 
 
 class O3GError(RuntimeError):

@@ -19,7 +19,9 @@ pytestmark = pytest.mark.gpu
 torch = pytest.importorskip("torch")
 GOLD = os.path.join(os.path.dirname(__file__), "golden")
 
-SEARCH = {"exact": 0, "balanced": 1, "prefilter": 2, "sorted": 3}
+# name -> {option: value}: O3G_OPT_SEARCH (1), O3G_OPT_PRUNE_MIN (10)
+SEARCH = {"exact": {1: 0}, "balanced": {1: 1}, "pruned": {1: 1, 10: 0}, "unpruned": {1: 1, 10: -2},
+          "prefilter": {1: 2}, "sorted": {1: 3}}
 GRID = {"dense": 1, "hashed": 2}
 
 
@@ -38,7 +40,8 @@ def _dev(a):
 
 def _ctx(o3g, w, search="balanced", grid="dense", order_T=None, src=None):
     ctx = o3g.Context(0)
-    ctx.set_option(1, SEARCH[search])
+    for opt, val in SEARCH[search].items():
+        ctx.set_option(opt, val)
     ctx.set_option(2, GRID[grid])
     ctx.set_target(_dev(w["target"]), _dev(w["target_normals"]), w["dmax"])
     ctx.set_source(_dev(w["source"] if src is None else src), order_T)
@@ -375,8 +378,8 @@ def test_cooperative_threshold_invariance(o3g, workloads, name):
     ref = oracle.step(T, w["source"], w["target"], w["target_normals"], w["dmax"],
                       grid=oracle.Grid(w["target"], w["dmax"]), subset=sub)
     outs = []
-    for cm in (1, 64, 0):
-        with _ctx(o3g, w, "balanced") as ctx:
+    for cm, search in ((1, "balanced"), (64, "balanced"), (0, "balanced"), (0, "pruned"), (64, "pruned")):
+        with _ctx(o3g, w, search) as ctx:
             ctx.set_option(6, cm)
             corr, st = _step(ctx, T, len(w["source"]))
         got = corr if sub is None else corr[sub]
@@ -424,3 +427,36 @@ def test_target_sort_invariance(o3g, workloads):
     assert np.array_equal(out[0][1]["terms"], out[1][1]["terms"])
     assert np.array_equal(out[0][2].transformation, out[1][2].transformation)
     assert out[0][3]["occupied_cells"] == out[1][3]["occupied_cells"]
+
+
+def test_row_pruning_face_stress(o3g):
+    """Row pruning near cell faces: targets and queries
+    placed within a few ulps of the grid's face planes, so the row lower
+    bounds are ~0 and own-row / face-row candidates tie or nearly tie."""
+    dmax = 0.125
+    h = dmax * (1 + 2.0 ** -20)
+    rs = Stream(77)
+    m = rs.integers(6000, 8).astype(np.float64)
+    base = rs.uniform(3 * 6000, 0.0, 1.0).reshape(-1, 3)
+    tgt = np.floor(base * 8) * h
+    tgt[:, 0] = base[:, 0]                                 # x free, y/z on face planes
+    jit = rs.integers(3 * 6000, 5).reshape(-1, 3) - 2      # -2..2 ulp
+    tgt = tgt.astype(np.float32)
+    for k in range(3):
+        for step in range(2):
+            sel = jit[:, k] > step
+            tgt[sel, k] = np.nextafter(tgt[sel, k], np.float32(2))
+            sel = jit[:, k] < -step
+            tgt[sel, k] = np.nextafter(tgt[sel, k], np.float32(-2))
+    tgt = np.concatenate([tgt, tgt[::5] + np.float32(0.25 * h)])
+    q = tgt[rs.integers(3000, len(tgt))] + (rs.uniform(3 * 3000, -1, 1).reshape(-1, 3) * 0.2 * h).astype(np.float32)
+    q[::3, 1] = tgt[rs.integers(1000, len(tgt)), 1]       # queries exactly on face planes
+    nrm = rs.unit_vectors(len(tgt)).astype(np.float32)
+    w = dict(source=q.astype(np.float32), target=tgt.astype(np.float32), target_normals=nrm, dmax=dmax)
+    ref = oracle.step(np.eye(4), w["source"], w["target"], nrm, dmax, grid=None)
+    assert (ref["corr"] >= 0).sum() > 1000
+    for search in ("pruned", "unpruned", "balanced"):
+        with _ctx(o3g, w, search) as ctx:
+            corr, st = _step(ctx, np.eye(4), len(q))
+        assert np.array_equal(corr, ref["corr"]), search
+        _terms_ok(st["terms"], ref)

@@ -16,6 +16,7 @@ ap.add_argument("--mode", default="run", choices=["run", "step"])
 ap.add_argument("--search", type=int, default=1)
 ap.add_argument("--bps", type=int, default=0)
 ap.add_argument("--coop-min", type=int, default=None)
+ap.add_argument("--prune-min", type=int, default=None)
 a = ap.parse_args()
 
 import torch  # noqa: E402
@@ -32,6 +33,8 @@ if a.bps:
     ctx.set_option(4, a.bps)
 if a.coop_min is not None:
     ctx.set_option(6, a.coop_min)
+if a.prune_min is not None:
+    ctx.set_option(10, a.prune_min)
 for _ in range(a.reps):
     ctx.set_target(tgt, nrm, w["dmax"])
     ctx.set_source(src, w["init_T"])

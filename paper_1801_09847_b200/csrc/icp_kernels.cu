@@ -20,7 +20,10 @@
 
 namespace o3g {
 
-constexpr int kP1Unroll = O3G_P1_UNROLL;   // pass-1 loop unroll (k3_balanced)
+constexpr int kP1Unroll = O3G_P1_UNROLL;
+#ifndef O3G_P1_PACKED
+#define O3G_P1_PACKED 1
+#endif   // pass-1 loop unroll (k3_balanced)
 
 // ------------------------------------------------------------------- K3
 template <bool PREFILTER, bool WRITE_CORR>
@@ -504,19 +507,31 @@ __global__ void __launch_bounds__(kK3Threads, 4) k3_balanced(const K3Args a) {
         int j1 = pj1;
         const int cl = heavy ? 0 : c - c0;   // (row pruning: the pre-scanned row is done)
         {
-            int k = k0;
-            int2 sg = cl > 0 ? segs[k0 * 32 + lane] : make_int2(0, 0);
+            // segment cursor as a shared-memory pointer (stride 32 int2); the
+            // x/y part of the distance in packed fp32x2 (FADD2/FMUL2):
+            // df = fma(uz, uz, fl(ux^2) + fl(uy^2)) has the same (1 +- 2^-24)^5
+            // two-sided bound as the scalar form (§5.2, §5.2c)
+            const int2* sp = segs + k0 * 32 + lane;
+            int2 sg = cl > 0 ? *sp : make_int2(0, 0);
             int j = sg.x, e = sg.y;
+            const float2 nsh = make_float2(-shx, -shy);
 #pragma unroll (kP1Unroll)
             for (int it = 0; it < cl; ++it) {
                 if (j == e) {
-                    ++k;
-                    sg = segs[k * 32 + lane];
+                    sp += 32;
+                    sg = *sp;
                     j = sg.x, e = sg.y;
                 }
                 const float4 t = __ldg(&a.tpos[j]);
+#if O3G_P1_PACKED
+                const float2 uxy = __fadd2_rn(make_float2(t.x, t.y), nsh);
+                const float2 sq = __fmul2_rn(uxy, uxy);
+                const float uz = t.z - shz;
+                const float df = fmaf(uz, uz, __fadd_rn(sq.x, sq.y));
+#else
                 const float ux = t.x - shx, uy = t.y - shy, uz = t.z - shz;
                 const float df = fmaf(uz, uz, fmaf(uy, uy, ux * ux));
+#endif
                 const bool lt = df < m1;
                 m2 = fminf(m2, lt ? m1 : df);
                 m1 = lt ? df : m1;

@@ -117,6 +117,10 @@ struct o3g_ctx {
     cudaStream_t user = nullptr;   // caller's stream (may be the legacy default)
     cudaStream_t exec = nullptr;   // internal capture/execution stream
     cudaEvent_t fence = nullptr;
+    // one-shot host inputs: H2D copies on their own stream, overlapped with
+    // the grid build (created on first use)
+    cudaStream_t copy = nullptr;
+    cudaEvent_t ev_copy[4] = {};
 
     // options
     int search = 1, grid_mode = 0, timing = 0, bps_override = 0, nbr_mask = 1, coop_min = -1;
@@ -134,7 +138,7 @@ struct o3g_ctx {
     DevBuf tpos, tnrm, cell_start, counts, nbr_a, nbr_b;
     bool nbr_ready = false;
     // scratch
-    DevBuf keys_a, keys_b, vals_a, vals_b, cub_tmp, stage_a, stage_b, misc;
+    DevBuf keys_a, keys_b, vals_a, vals_b, cub_tmp, stage_a, stage_b, stage_c, misc;
     // voxel_down_sample / multi-scale scratch
     DevBuf vk_a, vk_b, vflags, vrunid, vstarts, ms_src, ms_tgt, ms_nrm;
     DevBuf ev_T, ev_part, ev_out;
@@ -289,7 +293,7 @@ o3g_status o3g_destroy(o3g_ctx* c) {
     invalidate_graph(c);
     for (auto ev : c->events) cudaEventDestroy(ev);
     DevBuf* bufs[] = {&c->tpos, &c->tnrm, &c->cell_start, &c->counts, &c->nbr_a, &c->nbr_b, &c->keys_a, &c->keys_b,
-                      &c->vals_a, &c->vals_b, &c->cub_tmp, &c->stage_a, &c->stage_b, &c->misc,
+                      &c->vals_a, &c->vals_b, &c->cub_tmp, &c->stage_a, &c->stage_b, &c->stage_c, &c->misc,
                       &c->src4, &c->partials, &c->gathered, &c->state, &c->hist_fit, &c->hist_rmse,
                       &c->vk_a, &c->vk_b, &c->vflags, &c->vrunid, &c->vstarts, &c->ms_src,
                       &c->ms_tgt, &c->ms_nrm, &c->ev_T, &c->ev_part, &c->ev_out};
@@ -297,6 +301,9 @@ o3g_status o3g_destroy(o3g_ctx* c) {
     if (c->comm && nccl().comm_destroy) nccl().comm_destroy(c->comm);
     if (c->h_state) cudaFreeHost(c->h_state);
     if (c->fence) cudaEventDestroy(c->fence);
+    for (cudaEvent_t e : c->ev_copy)
+        if (e) cudaEventDestroy(e);
+    if (c->copy) cudaStreamDestroy(c->copy);
     if (c->exec) cudaStreamDestroy(c->exec);
     delete c;
     return O3G_OK;
@@ -345,8 +352,10 @@ o3g_status o3g_set_option(o3g_ctx* c, int option, int64_t value) {
     return O3G_OK;
 }
 
-o3g_status o3g_set_target(o3g_ctx* c, const float* xyz, const float* normals, int64_t n,
-                          double dmax) {
+// normals_ready (nullable): the normals arrive later on another stream; the
+// gather waits for it and their finiteness is checked at the final sync
+static o3g_status set_target_impl(o3g_ctx* c, const float* xyz, const float* normals, int64_t n,
+                                  double dmax, cudaEvent_t normals_ready) {
     if (!c) return fail(O3G_ERR_INVALID_ARGUMENT, "ctx is NULL");
     if (!xyz) return fail(O3G_ERR_INVALID_ARGUMENT, "target xyz is required");
     if (n <= 0 || n > 0x7ffffffeLL) return fail(O3G_ERR_INVALID_ARGUMENT, "n_target must be in [1, 2^31-2]");
@@ -369,8 +378,8 @@ o3g_status o3g_set_target(o3g_ctx* c, const float* xyz, const float* normals, in
     CK(cudaMemsetAsync(mm + 3, 0x00, 12 + 4 + 4 + 8, c->exec));
     CK(cudaMemsetAsync(mm + 12, 0x00, 4, c->exec));   // fused-tail block counter
     launch_bbox(dx, n, mm, bad, c->sms, c->exec);
-    if (dn) launch_check_finite(dn, 3 * n, bad, c->sms, c->exec);
-    c->launches += dn ? 2 : 1;
+    if (dn && !normals_ready) launch_check_finite(dn, 3 * n, bad, c->sms, c->exec);
+    c->launches += dn && !normals_ready ? 2 : 1;
     uint32_t h[8];
     CK(cudaMemcpyAsync(h, mm, 32, cudaMemcpyDeviceToHost, c->exec));
     CK(cudaStreamSynchronize(c->exec));
@@ -426,6 +435,13 @@ o3g_status o3g_set_target(o3g_ctx* c, const float* xyz, const float* normals, in
     TRY(c->cub_tmp.ensure(tmp));
     CK(cub::DeviceScan::ExclusiveSum(c->cub_tmp.p, tmp, c->counts.as<int32_t>(), c->cell_start.as<int32_t>(),
                                      (int)(g.table_size + 1), c->exec));
+    if (normals_ready) {
+        CK(cudaStreamWaitEvent(c->exec, normals_ready, 0));
+        if (dn) {
+            launch_check_finite(dn, 3 * n, bad, c->sms, c->exec);
+            c->launches += 1;
+        }
+    }
     if (radix) {   // stable (key, index) radix sort: cells in original-index order
         launch_gather_target(dx, dn, c->vals_b.as<int32_t>(), c->keys_b.as<uint32_t>(), n,
                              c->tpos.as<float4>(), c->tnrm.as<float4>(), occ, c->exec);
@@ -447,15 +463,23 @@ o3g_status o3g_set_target(o3g_ctx* c, const float* xyz, const float* normals, in
         c->nbr_ready = true;
     }
     unsigned long long h_occ = 0;
+    int32_t h_bad2 = 0;
     CK(cudaMemcpyAsync(&h_occ, occ, 8, cudaMemcpyDeviceToHost, c->exec));
+    if (normals_ready) CK(cudaMemcpyAsync(&h_bad2, bad, 4, cudaMemcpyDeviceToHost, c->exec));
     CK(cudaStreamSynchronize(c->exec));
     CK(cudaGetLastError());
+    if (h_bad2) return fail(O3G_ERR_INVALID_ARGUMENT, "non-finite target coordinate or normal");
     c->g = g;
     c->m = n;
     c->dmax = dmax;
     c->has_normals = dn != nullptr;
     c->occupied = (int64_t)h_occ;
     return O3G_OK;
+}
+
+o3g_status o3g_set_target(o3g_ctx* c, const float* xyz, const float* normals, int64_t n,
+                          double dmax) {
+    return set_target_impl(c, xyz, normals, n, dmax, nullptr);
 }
 
 o3g_status o3g_set_source(o3g_ctx* c, const float* xyz, int64_t n, const double order_T[16]) {
@@ -1002,6 +1026,42 @@ extern "C" o3g_status o3g_icp_multiscale(o3g_ctx* c, const float* src, int64_t n
     return O3G_OK;
 }
 
+// Host inputs: the three H2D copies run in order on the copy stream (target
+// xyz, normals, source) while the exec stream builds the grid as soon as the
+// target xyz has landed (the gather waits for the normals, the source
+// ordering for the source), so about 2/3 of the PCIe time hides the build.
+static o3g_status set_inputs(o3g_ctx* c, const float* src, int64_t ns, const float* tgt,
+                             const float* nrm, int64_t nt, double dmax, const double order_T[16]) {
+    const bool host = !is_device_ptr(src) && !is_device_ptr(tgt) && !(nrm && is_device_ptr(nrm));
+    if (!host || ns <= 0 || nt <= 0 || ns > 0x7ffffffeLL || nt > 0x7ffffffeLL) {
+        TRY(o3g_set_target(c, tgt, nrm, nt, dmax));
+        return o3g_set_source(c, src, ns, order_T);
+    }
+    CK(cudaSetDevice(c->device));
+    if (!c->copy) {
+        CK(cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking));
+        for (cudaEvent_t& e : c->ev_copy) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    TRY(c->stage_a.ensure((size_t)nt * 12));
+    if (nrm) TRY(c->stage_b.ensure((size_t)nt * 12));
+    TRY(c->stage_c.ensure((size_t)ns * 12));
+    // the staging buffers may still be read by earlier work on exec / user
+    TRY(enter(c));
+    CK(cudaEventRecord(c->ev_copy[3], c->exec));
+    CK(cudaStreamWaitEvent(c->copy, c->ev_copy[3], 0));
+    CK(cudaMemcpyAsync(c->stage_a.p, tgt, (size_t)nt * 12, cudaMemcpyHostToDevice, c->copy));
+    CK(cudaEventRecord(c->ev_copy[0], c->copy));
+    if (nrm) CK(cudaMemcpyAsync(c->stage_b.p, nrm, (size_t)nt * 12, cudaMemcpyHostToDevice, c->copy));
+    CK(cudaEventRecord(c->ev_copy[1], c->copy));
+    CK(cudaMemcpyAsync(c->stage_c.p, src, (size_t)ns * 12, cudaMemcpyHostToDevice, c->copy));
+    CK(cudaEventRecord(c->ev_copy[2], c->copy));
+    CK(cudaStreamWaitEvent(c->exec, c->ev_copy[0], 0));
+    TRY(set_target_impl(c, c->stage_a.as<float>(), nrm ? c->stage_b.as<float>() : nullptr, nt, dmax,
+                        c->ev_copy[1]));
+    CK(cudaStreamWaitEvent(c->exec, c->ev_copy[2], 0));
+    return o3g_set_source(c, c->stage_c.as<float>(), ns, order_T);
+}
+
 o3g_status o3g_icp_point_to_point(const float* source_xyz, int64_t n_source, const float* target_xyz,
                                   int64_t n_target, const double init_T[16], double dmax,
                                   int32_t max_iterations, double relative_fitness,
@@ -1018,8 +1078,7 @@ o3g_status o3g_icp_point_to_point(const float* source_xyz, int64_t n_source, con
     if (!c) TRY(o3g_create(&c, dev, cuda_stream));
     c->user = (cudaStream_t)cuda_stream;
     TRY(o3g_set_option(c, O3G_OPT_ESTIMATION, 1));
-    TRY(o3g_set_target(c, target_xyz, nullptr, n_target, dmax));
-    TRY(o3g_set_source(c, source_xyz, n_source, init_T));
+    TRY(set_inputs(c, source_xyz, n_source, target_xyz, nullptr, n_target, dmax, init_T));
     return o3g_icp_run(c, init_T, max_iterations, relative_fitness, relative_rmse, T_out, fitness,
                        inlier_rmse, info, nullptr, nullptr);
 }
@@ -1041,8 +1100,7 @@ o3g_status o3g_icp_point_to_plane(const float* source_xyz, int64_t n_source, con
     o3g_ctx*& c = cached[dev];
     if (!c) TRY(o3g_create(&c, dev, cuda_stream));
     c->user = (cudaStream_t)cuda_stream;
-    TRY(o3g_set_target(c, target_xyz, target_normals, n_target, dmax));
-    TRY(o3g_set_source(c, source_xyz, n_source, init_T));
+    TRY(set_inputs(c, source_xyz, n_source, target_xyz, target_normals, n_target, dmax, init_T));
     return o3g_icp_run(c, init_T, max_iterations, relative_fitness, relative_rmse, T_out, fitness,
                        inlier_rmse, info, nullptr, nullptr);
 }

@@ -460,3 +460,24 @@ def test_row_pruning_face_stress(o3g):
             corr, st = _step(ctx, np.eye(4), len(q))
         assert np.array_equal(corr, ref["corr"]), search
         _terms_ok(st["terms"], ref)
+
+
+def test_one_shot_overlapped_host_inputs(o3g, workloads):
+    """The one-shot call with host inputs copies target, normals and source on
+    a copy stream overlapped with the grid build; results equal the device
+    path, a non-finite normal (checked after the overlapped copy) is still
+    rejected, and the context recovers for the next call."""
+    w = workloads("depth")
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a, np.float32)).pin_memory()
+    a = o3g.icp_point_to_plane(pin(w["source"]), pin(w["target"]), pin(w["target_normals"]), w["dmax"],
+                               w["init_T"], w["iters"])
+    b = o3g.icp_point_to_plane(_dev(w["source"]), _dev(w["target"]), _dev(w["target_normals"]),
+                               w["dmax"], w["init_T"], w["iters"])
+    assert np.array_equal(a.transformation, b.transformation) and a.fitness == b.fitness
+    bad = w["target_normals"].copy()
+    bad[1234, 1] = np.nan
+    with pytest.raises(o3g.InvalidArgument):
+        o3g.icp_point_to_plane(pin(w["source"]), pin(w["target"]), pin(bad), w["dmax"], w["init_T"], 3)
+    c = o3g.icp_point_to_plane(w["source"], w["target"], w["target_normals"], w["dmax"],
+                               w["init_T"], w["iters"])
+    assert np.array_equal(c.transformation, b.transformation)

@@ -44,7 +44,7 @@ def parse():
     ap.add_argument("--impl", default="o3g", choices=["o3g", "reference"])
     ap.add_argument("--config", default="large16m")
     ap.add_argument("--iters", type=int, default=None)
-    ap.add_argument("--search", type=int, default=1, help="K3 variant: 0 exact fp64 scan, 1 two-pass warp (default), 2 single-pass prefilter, 3 tile-sorted two-pass")
+    ap.add_argument("--search", type=int, default=1, help="K3 variant: 0 exact fp64 scan, 1 two-pass warp (default), 2 single-pass prefilter, 3 tile-sorted two-pass, 4 smem-staged tiles")
     ap.add_argument("--coop-min", type=int, default=None, help="override O3G_OPT_COOP_MIN")
     ap.add_argument("--src-order", type=int, default=None, help="override O3G_OPT_SOURCE_ORDER")
     ap.add_argument("--prune-min", type=int, default=None, help="override O3G_OPT_PRUNE_MIN")
@@ -359,14 +359,14 @@ def main():
                        "scales": ([{"voxel": v, "dmax": d, "iters": k} for v, d, k in zip(vox, dms, its)]
                                   if multiscale else None),
                        "parallelism": f"source-shard x{world}, target grid replicated",
-                       "search": ["exact-fp64", "two-pass fp32-prefilter+exact-fp64", "single-pass fp32-prefilter+exact-fp64", "tile-sorted two-pass fp32-prefilter+exact-fp64"][a.search],
+                       "search": ["exact-fp64", "two-pass fp32-prefilter+exact-fp64", "single-pass fp32-prefilter+exact-fp64", "tile-sorted two-pass fp32-prefilter+exact-fp64", "smem-staged-tile two-pass fp32-prefilter+exact-fp64"][a.search],
                        "l2": (f"inputs {in_bytes / 1e6:.0f} MB < 126 MB L2: 256 MB write flushes L2 before "
                               "each timed step" if flush else
                               f"inputs {in_bytes / 1e6:.0f} MB > 126 MB L2 (no flush needed)")},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "traffic": traffic, "peak_kind": peak_kind,
                          "kernel": ["k3_corr_reduce<exact>", "k3_balanced", "k3_corr_reduce<prefilter>",
-                                    "k3_sorted"][a.search], "kernel_ms": k3_avg,
+                                    "k3_sorted", "k3_tiled"][a.search], "kernel_ms": k3_avg,
                          "alg_bytes_per_launch": alg_bytes},
             "cpu_baseline": cpu,
             "e2e": e2e,

@@ -85,10 +85,11 @@ __global__ void k_cell_keys(const float* __restrict__ xyz, int64_t n, GridDev g,
         int cy = min(max(cell_coord(sy, g.oy, g.inv_h, g.ny), 0), g.ny - 1);
         int cz = min(max(cell_coord(sz, g.oz, g.inv_h, g.nz), 0), g.nz - 1);
         uint32_t k;
-        if (brick) {   // source order: Morton order of 4x4x4-cell bricks, x-fastest inside
-            k = ((spread3((uint32_t)cx >> 2) | (spread3((uint32_t)cy >> 2) << 1) |
-                  (spread3((uint32_t)cz >> 2) << 2)) << 6) |
-                (((uint32_t)cz & 3u) << 4) | (((uint32_t)cy & 3u) << 2) | ((uint32_t)cx & 3u);
+        if (brick) {   // source order: Morton order of 2^b-cell bricks (b = brick), x-fastest inside
+            const uint32_t b = (uint32_t)brick, m = (1u << b) - 1u;
+            k = ((spread3((uint32_t)cx >> b) | (spread3((uint32_t)cy >> b) << 1) |
+                  (spread3((uint32_t)cz >> b) << 2)) << (3 * b)) |
+                (((uint32_t)cz & m) << (2 * b)) | (((uint32_t)cy & m) << b) | ((uint32_t)cx & m);
         } else {
             k = g.hashed ? ((grid_row_hash(cy, cz) + (uint32_t)cx) & g.hmask)
                          : (uint32_t)grid_index_dense(g, cx, cy, cz);
@@ -96,6 +97,24 @@ __global__ void k_cell_keys(const float* __restrict__ xyz, int64_t n, GridDev g,
         keys[i] = k;
         vals[i] = (int32_t)i;
     }
+}
+
+// tile starts of the (sorted) source: a new tile where the brick id (key >>
+// shift) changes (shift 32: never) and every `tq` queries inside a brick run.
+// run_start[i] = the start of i's run (an inclusive max-scan of these marks)
+__global__ void k_run_marks(const uint32_t* __restrict__ keys, int64_t n, int shift,
+                            int32_t* __restrict__ mark) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const bool start = i == 0 || (shift < 32 && (keys[i] >> shift) != (keys[i - 1] >> shift));
+        mark[i] = start ? (int32_t)i : 0;
+    }
+}
+__global__ void k_tile_flags(const int32_t* __restrict__ run_start, int64_t n, int tq,
+                             uint8_t* __restrict__ flag) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        flag[i] = ((i - run_start[i]) % tq) == 0;
 }
 
 __global__ void k_histogram(const uint32_t* __restrict__ keys, int64_t n, int32_t* counts,
@@ -209,6 +228,12 @@ void launch_cell_keys(const float* xyz, int64_t n, const GridDev& g, const doubl
     k_cell_keys<<<blocks_for(n, 256), 256, 0, s>>>(xyz, n, g, T != nullptr, t[0], t[1], t[2], t[3],
                                                    t[4], t[5], t[6], t[7], t[8], t[9], t[10], t[11],
                                                    keys, vals, brick);
+}
+void launch_run_marks(const uint32_t* keys, int64_t n, int shift, int32_t* mark, cudaStream_t s) {
+    k_run_marks<<<blocks_for(n, 256), 256, 0, s>>>(keys, n, shift, mark);
+}
+void launch_tile_flags(const int32_t* run_start, int64_t n, int tq, uint8_t* flag, cudaStream_t s) {
+    k_tile_flags<<<blocks_for(n, 256), 256, 0, s>>>(run_start, n, tq, flag);
 }
 void launch_histogram(const uint32_t* keys, int64_t n, int32_t* counts, unsigned long long* occupied,
                       cudaStream_t s) {

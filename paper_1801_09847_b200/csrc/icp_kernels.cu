@@ -685,6 +685,7 @@ int k3_max_blocks_per_sm(int variant, bool write_corr, int hashed, bool prune) {
         case 0: return write_corr ? occ_of<false, true>() : occ_of<false, false>();
         case 2: return write_corr ? occ_of<true, true>() : occ_of<true, false>();
         case 3: return k3_sorted_blocks_per_sm(write_corr, hashed);
+        case 4: return k3_tiled_blocks_per_sm(write_corr);
         default:   // the cooperative instantiation has the same footprint class
             if (prune) return write_corr ? occ_v2<true, false, true>(hashed) : occ_v2<false, false, true>(hashed);
             return write_corr ? occ_v2<true, false, false>(hashed) : occ_v2<false, false, false>(hashed);
@@ -702,6 +703,7 @@ void launch_k3(const K3Args& a, int blocks, int variant, bool write_corr, cudaSt
             else k3_corr_reduce<true, false><<<blocks, kK3Threads, 0, s>>>(a);
             break;
         case 3: launch_k3_sorted(a, blocks, write_corr, s); break;
+        case 4: launch_k3_tiled(a, blocks, write_corr, s); break;
         default: {
             const size_t sm = k3v2_smem(a.g.hashed);
             occ_v2<true, false, false>(a.g.hashed), occ_v2<false, false, false>(a.g.hashed);

@@ -7,6 +7,9 @@
 
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
+#include <cub/device/device_select.cuh>
+#include <cub/iterator/counting_input_iterator.cuh>
+#include <algorithm>
 #include <string>
 #include <vector>
 
@@ -146,6 +149,8 @@ struct o3g_ctx {
     int64_t n_total = 0, n_local = 0, shard_lo = 0;
     bool src_ready = false;
     DevBuf src4;
+    DevBuf tiles, tflag;  // variant 4 tile starts (local shard) and scratch
+    int32_t ntiles = 0;
     // loop
     DevBuf partials, gathered, state, hist_fit, hist_rmse;
     IcpState* h_state = nullptr;   // pinned
@@ -296,7 +301,7 @@ o3g_status o3g_destroy(o3g_ctx* c) {
                       &c->vals_a, &c->vals_b, &c->cub_tmp, &c->stage_a, &c->stage_b, &c->stage_c, &c->misc,
                       &c->src4, &c->partials, &c->gathered, &c->state, &c->hist_fit, &c->hist_rmse,
                       &c->vk_a, &c->vk_b, &c->vflags, &c->vrunid, &c->vstarts, &c->ms_src,
-                      &c->ms_tgt, &c->ms_nrm, &c->ev_T, &c->ev_part, &c->ev_out};
+                      &c->ms_tgt, &c->ms_nrm, &c->ev_T, &c->ev_part, &c->ev_out, &c->tiles, &c->tflag};
     for (DevBuf* b : bufs) b->release();
     if (c->comm && nccl().comm_destroy) nccl().comm_destroy(c->comm);
     if (c->h_state) cudaFreeHost(c->h_state);
@@ -313,7 +318,7 @@ o3g_status o3g_set_option(o3g_ctx* c, int option, int64_t value) {
     if (!c) return fail(O3G_ERR_INVALID_ARGUMENT, "ctx is NULL");
     switch (option) {
         case O3G_OPT_SEARCH:
-            if (value < 0 || value > 3) return fail(O3G_ERR_INVALID_ARGUMENT, "search must be in [0, 3]");
+            if (value < 0 || value > 4) return fail(O3G_ERR_INVALID_ARGUMENT, "search must be in [0, 4]");
             c->search = (int)value;
             break;
         case O3G_OPT_GRID:
@@ -508,15 +513,48 @@ o3g_status o3g_set_source(o3g_ctx* c, const float* xyz, int64_t n, const double 
     TRY(c->vals_b.ensure(n * 4));
     double T12[12];
     if (order_T) memcpy(T12, order_T, sizeof(T12));
-    const bool brick = c->src_order == 1 && !c->g.hashed && c->g.nx <= 4096 && c->g.ny <= 4096 &&
-                       c->g.nz <= 4096;
+    // order: 8^3-cell brick Morton for the staged-tile kernel (variant 4),
+    // 4^3 bricks for O3G_OPT_SOURCE_ORDER = 1, else by cell; brick keys must
+    // fit 32 bits (3 * bits(dim >> b) + 3 b)
+    int brick = c->g.hashed ? 0 : c->search == 4 ? 3 : c->src_order == 1 ? 2 : 0;
+    if (brick) {
+        const int dmaxc = std::max(c->g.nx, std::max(c->g.ny, c->g.nz));
+        if (3 * bits_for((uint64_t)(dmaxc >> brick)) + 3 * brick > 32) brick = 0;
+    }
     launch_cell_keys(dx, n, c->g, order_T ? T12 : nullptr, c->keys_a.as<uint32_t>(),
-                     c->vals_a.as<int32_t>(), c->exec, brick ? 1 : 0);
+                     c->vals_a.as<int32_t>(), c->exec, brick);
     TRY(sort_pairs(c, n, brick ? 32 : bits_for((uint64_t)(c->g.table_size - 1))));
     const int64_t lo = (int64_t)c->rank * n / c->world, hi = (int64_t)(c->rank + 1) * n / c->world;
     TRY(c->src4.ensure((size_t)(hi - lo > 0 ? hi - lo : 1) * sizeof(float4)));
     if (hi > lo) launch_gather_source(dx, c->vals_b.as<int32_t>(), lo, hi, c->src4.as<float4>(), c->exec);
     c->launches += 3;
+    c->ntiles = 0;
+    if (c->search == 4 && !c->g.hashed && hi > lo) {
+        // variant 4 tiles: a new tile at every 8^3-brick change and every
+        // kTileQ queries inside a brick (deterministic: scan + stable select)
+        const int64_t nl = hi - lo;
+        int32_t* mark = c->vals_a.as<int32_t>();
+        int32_t* run_start = (int32_t*)c->keys_a.p;
+        TRY(c->tflag.ensure((size_t)nl + 64));
+        TRY(c->tiles.ensure((size_t)(nl + 1) * 4));
+        launch_run_marks(c->keys_b.as<uint32_t>() + lo, nl, brick == 3 ? 9 : 32, mark, c->exec);
+        size_t tmp = 0;
+        CK(cub::DeviceScan::InclusiveScan(nullptr, tmp, mark, run_start, cub::Max(), (int)nl, c->exec));
+        TRY(c->cub_tmp.ensure(tmp));
+        CK(cub::DeviceScan::InclusiveScan(c->cub_tmp.p, tmp, mark, run_start, cub::Max(), (int)nl, c->exec));
+        uint8_t* flag = c->tflag.as<uint8_t>();
+        launch_tile_flags(run_start, nl, kTileQ, flag, c->exec);
+        TRY(c->misc.ensure(128));
+        int32_t* nsel = (int32_t*)(c->misc.as<uint32_t>() + 20);
+        tmp = 0;
+        CK(cub::DeviceSelect::Flagged(nullptr, tmp, cub::CountingInputIterator<int32_t>(0), flag,
+                                      c->tiles.as<int32_t>(), nsel, (int)nl, c->exec));
+        TRY(c->cub_tmp.ensure(tmp));
+        CK(cub::DeviceSelect::Flagged(c->cub_tmp.p, tmp, cub::CountingInputIterator<int32_t>(0), flag,
+                                      c->tiles.as<int32_t>(), nsel, (int)nl, c->exec));
+        CK(cudaMemcpyAsync(&c->ntiles, nsel, 4, cudaMemcpyDeviceToHost, c->exec));
+        c->launches += 5;
+    }
     CK(cudaStreamSynchronize(c->exec));
     CK(cudaGetLastError());
     c->n_total = n;
@@ -546,7 +584,10 @@ static int prune_of(const o3g_ctx* c) {
 }
 
 // point-to-point runs on the two-pass kernel
-static int k3_variant(const o3g_ctx* c) { return c->estimation ? 1 : c->search; }
+// (variant 4 stages a dense-table halo: a hashed grid runs variant 1)
+static int k3_variant(const o3g_ctx* c) {
+    return c->estimation || (c->search == 4 && (c->g.hashed || c->ntiles <= 0)) ? 1 : c->search;
+}
 
 static int k3_blocks(o3g_ctx* c, bool write_corr) {
     int bps = c->bps_override ? c->bps_override : k3_max_blocks_per_sm(k3_variant(c), write_corr, c->g.hashed, prune_of(c) >= 0);
@@ -586,6 +627,8 @@ static K3Args k3_args(o3g_ctx* c, int32_t* corr) {
     a.eval_T = nullptr;
     a.n_eval = 0;
     a.coop_min = coop_min_of(c);
+    a.tiles = c->tiles.as<int32_t>();
+    a.ntiles = c->ntiles;
     a.prune_min = prune_of(c);
     a.prune = a.prune_min >= 0;
     if (!a.prune) a.prune_min = 0;

@@ -88,6 +88,8 @@ void launch_check_finite(const float* v, int64_t count, int32_t* nonfinite, int 
 // needs < 2^10 bricks per axis), 0: the table index
 void launch_cell_keys(const float* xyz, int64_t n, const GridDev& g, const double* T12_or_null,
                       uint32_t* keys, int32_t* vals, cudaStream_t s, int brick = 0);
+void launch_run_marks(const uint32_t* keys, int64_t n, int shift, int32_t* mark, cudaStream_t s);
+void launch_tile_flags(const int32_t* run_start, int64_t n, int tq, uint8_t* flag, cudaStream_t s);
 void launch_histogram(const uint32_t* keys, int64_t n, int32_t* counts, unsigned long long* occupied,
                       cudaStream_t s);
 void launch_scatter_target(const float* xyz, const float* nrm, const uint32_t* keys, int64_t n,
@@ -140,6 +142,8 @@ struct K3Args {
                                // (nullable); partials at [(y * gridDim.x + x) * 32]
     int coop_min;              // variant 1: queries with >= coop_min candidates are
                                // scanned by the whole warp (0 = never)
+    const int32_t* tiles;      // variant 4: tile starts in the local source (ntiles)
+    int32_t ntiles;
     int prune;                 // variant 1: row-pruning instantiation (dense grid)
     int prune_min;             //   ... for light queries with >= prune_min candidates
     // fused tail (single GPU, variant 1): the last block to finish reduces the
@@ -153,7 +157,10 @@ struct K3Args {
 // variant: 0 = exact fp64 scan (k3_corr_reduce), 1 = two-pass warp kernel
 // (k3_balanced), 2 = single-pass prefilter (k3_corr_reduce<true>), 3 = tile-sorted
 // two-pass kernel (k3_sorted, default). Identical correspondences.
-inline int k3_threads(int variant) { return variant == 3 ? 128 : kK3Threads; }
+constexpr int kTileQ = 128;       // variant 4: queries per tile (max)
+inline int k3_threads(int variant) { return variant == 3 ? 128 : variant == 4 ? kTileQ : kK3Threads; }
+int k3_tiled_blocks_per_sm(bool write_corr);
+void launch_k3_tiled(const K3Args& a, int blocks, bool write_corr, cudaStream_t s);
 int k3_sorted_blocks_per_sm(bool write_corr, int hashed);
 void launch_k3_sorted(const K3Args& a, int blocks, bool write_corr, cudaStream_t s);
 void launch_k3(const K3Args& a, int blocks, int variant, bool write_corr, cudaStream_t s);

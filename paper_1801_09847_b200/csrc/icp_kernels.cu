@@ -237,6 +237,8 @@ __global__ void __launch_bounds__(kK3Threads, 4) k3_balanced(const K3Args a) {
     // full search runs on full warps of live queries only.
     __shared__ int qbuf[kK3Threads / 32][64];
     const bool use_queue = a.nbr_bits != nullptr;
+    __shared__ float4 s_gap[PRUNE && COOP ? kK3Threads / 32 : 1][32];
+    __shared__ int s_rmask[PRUNE && COOP ? kK3Threads / 32 : 1][32];
     int qn = 0;   // warp-uniform queue length
     int base = gw * 32;
     for (;;) {
@@ -286,6 +288,10 @@ __global__ void __launch_bounds__(kK3Threads, 4) k3_balanced(const K3Args a) {
         // pass 1 then starts at segment k0
         float pm1 = CUDART_INF_F, pm2 = CUDART_INF_F;
         int pj1 = -1, k0 = 0, c0 = 0;
+        // (PRUNE) face gaps of the query's cell and the kOrder positions of the
+        // staged rows (bit t) go to shared memory for the cooperative path
+        float gym = 0.f, gyp = 0.f, gzm = 0.f, gzp = 0.f;
+        int rmask = 0;
         float4 p = make_float4(0.f, 0.f, 0.f, 0.f);
         if (i < a.n) {
             p = __ldg(&a.src[i]);
@@ -344,8 +350,12 @@ __global__ void __launch_bounds__(kK3Threads, 4) k3_balanced(const K3Args a) {
                         if (ee[r] > bb[r]) fb = bb[r], fe = ee[r];
                     }
                     float ub = CUDART_INF_F;
-                    float gym = 0.f, gyp = 0.f, gzm = 0.f, gzp = 0.f;
-                    if (tot >= a.prune_min && !(COOP && tot >= a.coop_min) && fe > fb) {
+                    if (tot >= a.prune_min || (COOP && tot >= a.coop_min)) {
+                        face_gaps(sy, g.oy, g.h, cy, gym, gyp);
+                        face_gaps(sz, g.oz, g.h, cz, gzm, gzp);
+                    }
+                    // (the cooperative instantiation prunes heavy queries only)
+                    if (!COOP && tot >= a.prune_min && fe > fb) {
                         // that row first: the same prefilter scan as pass 1
                         for (int j = fb; j < fe; ++j) {
                             const float4 t = __ldg(&a.tpos[j]);
@@ -359,8 +369,6 @@ __global__ void __launch_bounds__(kK3Threads, 4) k3_balanced(const K3Args a) {
                         k0 = 1;
                         c0 = fe - fb;
                         ub = prune_ub(pm1, __double2float_ru(E1), r2u);
-                        face_gaps(sy, g.oy, g.h, cy, gym, gyp);
-                        face_gaps(sz, g.oz, g.h, cz, gzm, gzp);
                     }
                     // own row first, then the 4 face rows, then the 4 corner rows;
                     // rows provably farther than the pre-scanned best are not
@@ -375,7 +383,12 @@ __global__ void __launch_bounds__(kK3Threads, 4) k3_balanced(const K3Args a) {
                             segs[nseg * 32 + lane] = make_int2(bb[r], ee[r]);
                             ++nseg;
                             c += ee[r] - bb[r];
+                            rmask |= 1 << t;
                         }
+                    }
+                    if (COOP) {
+                        s_gap[PRUNE ? warp : 0][lane] = make_float4(gym, gyp, gzm, gzp);
+                        s_rmask[PRUNE ? warp : 0][lane] = rmask;
                     }
                 }
             } else if (g.hashed && near) {
@@ -433,7 +446,19 @@ __global__ void __launch_bounds__(kK3Threads, 4) k3_balanced(const K3Args a) {
             const int qseg = __shfl_sync(0xffffffffu, nseg, q);
             float lm1 = CUDART_INF_F, lm2 = CUDART_INF_F;
             int lj1 = INT_MAX;
-            for (int k = 0; k < qseg; ++k) {
+            // (PRUNE, dense) rows in kOrder: after each row the warp merges its
+            // state, and a later row whose lower bound exceeds ub(m1) is
+            // skipped (§5.2c; warp-uniform decisions)
+            const bool cprune = PRUNE && !g.hashed;
+            int qmask = 0;
+            float qgym = 0.f, qgyp = 0.f, qgzm = 0.f, qgzp = 0.f, qE1u = 0.f;
+            if (cprune) {   // (a heavy query is near and dense: its slots were written)
+                qmask = s_rmask[PRUNE ? warp : 0][q];
+                const float4 gq = s_gap[PRUNE ? warp : 0][q];
+                qgym = gq.x, qgyp = gq.y, qgzm = gq.z, qgzp = gq.w;
+                qE1u = __double2float_ru(__shfl_sync(0xffffffffu, E1, q));
+            }
+            for (int k = 0; !cprune && k < qseg; ++k) {   // plain: every row, one merge at the end
                 const int2 sg = segs[k * 32 + q];
 #pragma unroll 4
                 for (int j = sg.x + lane; j < sg.y; j += 32) {
@@ -446,15 +471,52 @@ __global__ void __launch_bounds__(kK3Threads, 4) k3_balanced(const K3Args a) {
                     lj1 = lt ? j : lj1;
                 }
             }
+            for (int k = 0; cprune && k < qseg; ++k) {
+                const int t = __ffs(qmask) - 1;
+                qmask &= qmask - 1;
+                const int r = (int)((0x862075314ull >> (4 * t)) & 0xFull);   // kOrder[t]
+                if (k > 0 &&
+                    row_lower(r % 3 - 1, r / 3 - 1, qgym, qgyp, qgzm, qgzp) > prune_ub(lm1, qE1u, r2u))
+                    continue;
+                const int2 sg = segs[k * 32 + q];
+                float n1 = CUDART_INF_F, n2 = CUDART_INF_F;
+                int nj = INT_MAX;
+#pragma unroll 4
+                for (int j = sg.x + lane; j < sg.y; j += 32) {
+                    const float4 t4 = __ldg(&a.tpos[j]);
+                    const float ux = t4.x - qx, uy = t4.y - qy, uz = t4.z - qz;
+                    const float df = fmaf(uz, uz, fmaf(uy, uy, ux * ux));
+                    const bool lt = df < n1;
+                    n2 = fminf(n2, lt ? n1 : df);
+                    n1 = lt ? df : n1;
+                    nj = lt ? j : nj;
+                }
 #pragma unroll
-            for (int o = 16; o; o >>= 1) {   // (m1, j1) lexicographic min; m2 = 2nd smallest
-                const float om1 = __shfl_xor_sync(0xffffffffu, lm1, o);
-                const float om2 = __shfl_xor_sync(0xffffffffu, lm2, o);
-                const int oj1 = __shfl_xor_sync(0xffffffffu, lj1, o);
-                lm2 = fminf(fminf(lm2, om2), fmaxf(lm1, om1));
-                const bool take = om1 < lm1 || (om1 == lm1 && oj1 < lj1);
-                lj1 = take ? oj1 : lj1;
-                lm1 = fminf(lm1, om1);
+                for (int o = 16; o; o >>= 1) {   // this row's (m1, j1, m2) on every lane
+                    const float om1 = __shfl_xor_sync(0xffffffffu, n1, o);
+                    const float om2 = __shfl_xor_sync(0xffffffffu, n2, o);
+                    const int oj1 = __shfl_xor_sync(0xffffffffu, nj, o);
+                    n2 = fminf(fminf(n2, om2), fmaxf(n1, om1));
+                    const bool take = om1 < n1 || (om1 == n1 && oj1 < nj);
+                    nj = take ? oj1 : nj;
+                    n1 = fminf(n1, om1);
+                }
+                lm2 = fminf(fminf(lm2, n2), fmaxf(lm1, n1));   // merge into the (uniform) total
+                const bool take = n1 < lm1 || (n1 == lm1 && nj < lj1);
+                lj1 = take ? nj : lj1;
+                lm1 = fminf(lm1, n1);
+            }
+            if (!cprune) {
+#pragma unroll
+                for (int o = 16; o; o >>= 1) {   // (m1, j1) lexicographic min; m2 = 2nd smallest
+                    const float om1 = __shfl_xor_sync(0xffffffffu, lm1, o);
+                    const float om2 = __shfl_xor_sync(0xffffffffu, lm2, o);
+                    const int oj1 = __shfl_xor_sync(0xffffffffu, lj1, o);
+                    lm2 = fminf(fminf(lm2, om2), fmaxf(lm1, om1));
+                    const bool take = om1 < lm1 || (om1 == lm1 && oj1 < lj1);
+                    lj1 = take ? oj1 : lj1;
+                    lm1 = fminf(lm1, om1);
+                }
             }
             const double qsx = __shfl_sync(0xffffffffu, sx, q), qsy = __shfl_sync(0xffffffffu, sy, q),
                          qsz = __shfl_sync(0xffffffffu, sz, q), qE1 = __shfl_sync(0xffffffffu, E1, q);

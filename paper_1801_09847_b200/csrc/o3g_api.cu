@@ -580,7 +580,8 @@ static int prune_of(const o3g_ctx* c) {
     if (c->g.hashed || c->prune_min == -2) return -1;
     if (c->prune_min >= 0) return c->prune_min;
     const double rho = (double)c->m / (double)(c->occupied > 0 ? c->occupied : 1);
-    return rho >= 4.0 && rho < 32.0 ? 32 : -1;
+    // >= 32 per cell: the cooperative path prunes its rows; no light pre-scan
+    return rho >= 32.0 ? (1 << 30) : rho >= 4.0 ? 32 : -1;
 }
 
 // point-to-point runs on the two-pass kernel

@@ -48,6 +48,7 @@ def parse():
     ap.add_argument("--coop-min", type=int, default=None, help="override O3G_OPT_COOP_MIN")
     ap.add_argument("--src-order", type=int, default=None, help="override O3G_OPT_SOURCE_ORDER")
     ap.add_argument("--prune-min", type=int, default=None, help="override O3G_OPT_PRUNE_MIN")
+    ap.add_argument("--interleave", type=int, default=None, help="override O3G_OPT_INTERLEAVE")
     ap.add_argument("--bps", type=int, default=None, help="override O3G_OPT_BLOCKS_PER_SM")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -210,6 +211,8 @@ def main():
         ctx.set_option(8, a.src_order)
     if a.prune_min is not None:
         ctx.set_option(10, a.prune_min)
+    if a.interleave is not None:
+        ctx.set_option(11, a.interleave)
     if a.bps is not None:
         ctx.set_option(4, a.bps)
     if world > 1:

@@ -245,10 +245,13 @@ __global__ void __launch_bounds__(kK3Threads, 4) k3_balanced(const K3Args a) {
         int i;
         if (use_queue) {
         while (qn < 32 && base < a.n) {
-            const int i0 = base + lane;
+            // interleaved batches (a.ilv = number of batches): lane l of batch b
+            // takes query l * ilv + b, so queries that cluster in the ordered
+            // source (LiDAR points next to the sensor) spread over all warps
+            const int i0 = a.ilv ? min(lane * a.ilv + (base >> 5), a.n) : base + lane;
             base += nw * 32;
             // the warp's next source batch: in flight while this one is processed
-            if (base + lane < a.n) asm volatile("prefetch.global.L1 [%0];" ::"l"(a.src + base + lane));
+            if (!a.ilv && base + lane < a.n) asm volatile("prefetch.global.L1 [%0];" ::"l"(a.src + base + lane));
             bool live = false;
             if (i0 < a.n) {
                 const float4 p0 = __ldg(&a.src[i0]);
@@ -278,7 +281,7 @@ __global__ void __launch_bounds__(kK3Threads, 4) k3_balanced(const K3Args a) {
         qn -= take;
         } else {
             if (base >= a.n) break;
-            i = base + lane;
+            i = a.ilv ? min(lane * a.ilv + (base >> 5), a.n) : base + lane;
             base += nw * 32;
         }
         double sx = 0.0, sy = 0.0, sz = 0.0, E1 = 0.0;

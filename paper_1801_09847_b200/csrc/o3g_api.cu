@@ -131,6 +131,7 @@ struct o3g_ctx {
     int src_order = 0;    // 0 lexicographic cell, 1 brick-Morton
     int target_sort = 1;  // 0 counting sort, 1 stable radix sort (default: measured faster)
     int prune_min = -1;   // variant 1 row pruning: -1 auto, -2 never, >= 0 threshold
+    int interleave = -1;  // variant 1 batch interleave: -1 auto, 0 off, 1 on
     bool has_normals = false;
 
     // target grid
@@ -334,6 +335,10 @@ o3g_status o3g_set_option(o3g_ctx* c, int option, int64_t value) {
         case O3G_OPT_TARGET_SORT:
             if (value < 0 || value > 1) return fail(O3G_ERR_INVALID_ARGUMENT, "target sort must be 0 or 1");
             c->target_sort = (int)value;
+            break;
+        case O3G_OPT_INTERLEAVE:
+            if (value < -1 || value > 1) return fail(O3G_ERR_INVALID_ARGUMENT, "interleave must be -1, 0 or 1");
+            c->interleave = (int)value;
             break;
         case O3G_OPT_PRUNE_MIN:
             if (value < -2 || value > (1 << 30)) return fail(O3G_ERR_INVALID_ARGUMENT, "prune_min out of range");
@@ -630,6 +635,10 @@ static K3Args k3_args(o3g_ctx* c, int32_t* corr) {
     a.coop_min = coop_min_of(c);
     a.tiles = c->tiles.as<int32_t>();
     a.ntiles = c->ntiles;
+    // interleave: auto with the cooperative path (dense targets: heavy
+    // queries cluster in the ordered source and would serialise a few warps)
+    const bool ilv = c->interleave == 1 || (c->interleave == -1 && coop_min_of(c) > 0);
+    a.ilv = ilv ? (int)((c->n_local + 31) / 32) : 0;
     a.prune_min = prune_of(c);
     a.prune = a.prune_min >= 0;
     if (!a.prune) a.prune_min = 0;

@@ -144,6 +144,7 @@ struct K3Args {
                                // scanned by the whole warp (0 = never)
     const int32_t* tiles;      // variant 4: tile starts in the local source (ntiles)
     int32_t ntiles;
+    int ilv;                   // variant 1: 0, or interleaved batches (= ceil(n / 32))
     int prune;                 // variant 1: row-pruning instantiation (dense grid)
     int prune_min;             //   ... for light queries with >= prune_min candidates
     // fused tail (single GPU, variant 1): the last block to finish reduces the

@@ -17,6 +17,7 @@ ap.add_argument("--search", type=int, default=1)
 ap.add_argument("--bps", type=int, default=0)
 ap.add_argument("--coop-min", type=int, default=None)
 ap.add_argument("--prune-min", type=int, default=None)
+ap.add_argument("--interleave", type=int, default=None)
 a = ap.parse_args()
 
 import torch  # noqa: E402
@@ -35,6 +36,8 @@ if a.coop_min is not None:
     ctx.set_option(6, a.coop_min)
 if a.prune_min is not None:
     ctx.set_option(10, a.prune_min)
+if a.interleave is not None:
+    ctx.set_option(11, a.interleave)
 for _ in range(a.reps):
     ctx.set_target(tgt, nrm, w["dmax"])
     ctx.set_source(src, w["init_T"])

@@ -49,6 +49,7 @@ def parse():
     ap.add_argument("--src-order", type=int, default=None, help="override O3G_OPT_SOURCE_ORDER")
     ap.add_argument("--prune-min", type=int, default=None, help="override O3G_OPT_PRUNE_MIN")
     ap.add_argument("--interleave", type=int, default=None, help="override O3G_OPT_INTERLEAVE")
+    ap.add_argument("--xsort", type=int, default=None, help="override O3G_OPT_XSORT")
     ap.add_argument("--bps", type=int, default=None, help="override O3G_OPT_BLOCKS_PER_SM")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -213,6 +214,8 @@ def main():
         ctx.set_option(10, a.prune_min)
     if a.interleave is not None:
         ctx.set_option(11, a.interleave)
+    if a.xsort is not None:
+        ctx.set_option(12, a.xsort)
     if a.bps is not None:
         ctx.set_option(4, a.bps)
     if world > 1:

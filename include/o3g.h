@@ -257,11 +257,15 @@ o3g_status o3g_dist_init(o3g_ctx* ctx, int rank, int world, const void* nccl_uni
  *   queries of the ordered source per warp batch; 1 = lane l of batch b
  *   takes query l * ceil(n/32) + b (spreads clustered heavy queries over
  *   all warps); -1 = auto (default: on when the cooperative path is).
+ * O3G_OPT_XSORT: order the target by x inside each cell (set at the next
+ *   o3g_set_target) so the cooperative path scans, per x-row, only the
+ *   window |q_x - s'_x| <= sqrt(ub - L) found by a warp-wide search
+ *   (DESIGN.md §5.2c); -1 = auto (default: >= 32 points per occupied cell).
  * Results are identical for every value of the other options.           */
 enum { O3G_OPT_SEARCH = 1, O3G_OPT_GRID = 2, O3G_OPT_TIMING = 3, O3G_OPT_BLOCKS_PER_SM = 4,
        O3G_OPT_NBR_MASK = 5, O3G_OPT_COOP_MIN = 6, O3G_OPT_ESTIMATION = 7,
        O3G_OPT_SOURCE_ORDER = 8, O3G_OPT_TARGET_SORT = 9, O3G_OPT_PRUNE_MIN = 10,
-       O3G_OPT_INTERLEAVE = 11 };
+       O3G_OPT_INTERLEAVE = 11, O3G_OPT_XSORT = 12 };
 o3g_status o3g_set_option(o3g_ctx* ctx, int option, int64_t value);
 
 /* Sum of the correspondence-kernel (K3) durations of the last o3g_icp_run

@@ -99,6 +99,33 @@ __global__ void k_cell_keys(const float* __restrict__ xyz, int64_t n, GridDev g,
     }
 }
 
+// x-order inside cells (O3G_OPT_XSORT): key = cell << 32 | order-preserving
+// bits of x, value = current position; then the target is permuted
+__global__ void k_xkeys(const float4* __restrict__ tpos, int64_t n, GridDev g, uint64_t* __restrict__ keys,
+                        int32_t* __restrict__ vals) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const float4 p = tpos[i];
+        const int cx = min(max(cell_coord((double)p.x, g.ox, g.inv_h, g.nx), 0), g.nx - 1);
+        const int cy = min(max(cell_coord((double)p.y, g.oy, g.inv_h, g.ny), 0), g.ny - 1);
+        const int cz = min(max(cell_coord((double)p.z, g.oz, g.inv_h, g.nz), 0), g.nz - 1);
+        uint32_t u = __float_as_uint(p.x);
+        u = (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+        keys[i] = ((uint64_t)grid_index_dense(g, cx, cy, cz) << 32) | u;
+        vals[i] = (int32_t)i;
+    }
+}
+__global__ void k_permute_target(const float4* __restrict__ tpos, const float4* __restrict__ tnrm,
+                                 const int32_t* __restrict__ perm, int64_t n, float4* __restrict__ opos,
+                                 float4* __restrict__ onrm) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t v = perm[i];
+        opos[i] = tpos[v];
+        onrm[i] = tnrm[v];
+    }
+}
+
 // tile starts of the (sorted) source: a new tile where the brick id (key >>
 // shift) changes (shift 32: never) and every `tq` queries inside a brick run.
 // run_start[i] = the start of i's run (an inclusive max-scan of these marks)
@@ -228,6 +255,14 @@ void launch_cell_keys(const float* xyz, int64_t n, const GridDev& g, const doubl
     k_cell_keys<<<blocks_for(n, 256), 256, 0, s>>>(xyz, n, g, T != nullptr, t[0], t[1], t[2], t[3],
                                                    t[4], t[5], t[6], t[7], t[8], t[9], t[10], t[11],
                                                    keys, vals, brick);
+}
+void launch_xkeys(const float4* tpos, int64_t n, const GridDev& g, uint64_t* keys, int32_t* vals,
+                  cudaStream_t s) {
+    k_xkeys<<<blocks_for(n, 256), 256, 0, s>>>(tpos, n, g, keys, vals);
+}
+void launch_permute_target(const float4* tpos, const float4* tnrm, const int32_t* perm, int64_t n,
+                           float4* opos, float4* onrm, cudaStream_t s) {
+    k_permute_target<<<blocks_for(n, 256), 256, 0, s>>>(tpos, tnrm, perm, n, opos, onrm);
 }
 void launch_run_marks(const uint32_t* keys, int64_t n, int shift, int32_t* mark, cudaStream_t s) {
     k_run_marks<<<blocks_for(n, 256), 256, 0, s>>>(keys, n, shift, mark);

@@ -207,6 +207,25 @@ __device__ __forceinline__ float row_lower(int dy, int dz, float gym, float gyp,
     return __fadd_rd(la, lb);
 }
 
+// x-windows (x-sorted target, cooperative path): first index in [lo, hi) whose
+// x is >= v (GE) or > v (!GE); x ascends along an x-row. 32-ary warp search.
+template <bool GE>
+__device__ __forceinline__ int warp_bound_x(const float4* __restrict__ tpos, int lo, int hi, float v, int lane) {
+    while (hi - lo > 32) {
+        const int step = (hi - lo + 31) >> 5;
+        const int p = lo + lane * step;
+        const float x = p < hi ? __ldg(&tpos[p].x) : CUDART_INF_F;
+        const int cnt = __popc(__ballot_sync(0xffffffffu, p < hi && (GE ? x < v : x <= v)));
+        if (cnt == 0) return lo;
+        const int nlo = lo + (cnt - 1) * step + 1;
+        hi = min(hi, lo + cnt * step + 1);
+        lo = nlo;
+    }
+    const int p = lo + lane;
+    const float x = p < hi ? __ldg(&tpos[p].x) : CUDART_INF_F;
+    return lo + __popc(__ballot_sync(0xffffffffu, p < hi && (GE ? x < v : x <= v)));
+}
+
 __device__ __noinline__ void tail_finish(const double* terms, IcpState* st, double* hist_fit, double* hist_rmse,
                             int mode);
 
@@ -455,7 +474,9 @@ __global__ void __launch_bounds__(kK3Threads, 4) k3_balanced(const K3Args a) {
             const bool cprune = PRUNE && !g.hashed;
             int qmask = 0;
             float qgym = 0.f, qgyp = 0.f, qgzm = 0.f, qgzp = 0.f, qE1u = 0.f;
+            double qsxw = 0.0;
             if (cprune) {   // (a heavy query is near and dense: its slots were written)
+                qsxw = __shfl_sync(0xffffffffu, sx, q);
                 qmask = s_rmask[PRUNE ? warp : 0][q];
                 const float4 gq = s_gap[PRUNE ? warp : 0][q];
                 qgym = gq.x, qgyp = gq.y, qgzm = gq.z, qgzp = gq.w;
@@ -478,10 +499,20 @@ __global__ void __launch_bounds__(kK3Threads, 4) k3_balanced(const K3Args a) {
                 const int t = __ffs(qmask) - 1;
                 qmask &= qmask - 1;
                 const int r = (int)((0x862075314ull >> (4 * t)) & 0xFull);   // kOrder[t]
-                if (k > 0 &&
-                    row_lower(r % 3 - 1, r / 3 - 1, qgym, qgyp, qgzm, qgzp) > prune_ub(lm1, qE1u, r2u))
-                    continue;
-                const int2 sg = segs[k * 32 + q];
+                const float Lr = row_lower(r % 3 - 1, r / 3 - 1, qgym, qgyp, qgzm, qgzp);
+                const float ub = prune_ub(lm1, qE1u, r2u);
+                if (k > 0 && Lr > ub) continue;
+                int2 sg = segs[k * 32 + q];
+                if (a.xsorted) {
+                    // only |q_x - s'_x| <= w can have d^2 <= ub: d^2 >= dx^2 + L_row
+                    float w;
+                    asm("sqrt.approx.f32 %0, %1;" : "=f"(w) : "f"(fmaxf(__fsub_ru(ub, Lr), 0.f)));
+                    w = __fadd_ru(__fmul_ru(w, 1.0f + 1.52587890625e-05f), 2e-19f);
+                    const float lox = __double2float_rd(__dsub_rd(qsxw, (double)w));
+                    const float hix = __double2float_ru(__dadd_ru(qsxw, (double)w));
+                    sg.x = warp_bound_x<true>(a.tpos, sg.x, sg.y, lox, lane);
+                    sg.y = warp_bound_x<false>(a.tpos, sg.x, sg.y, hix, lane);
+                }
                 float n1 = CUDART_INF_F, n2 = CUDART_INF_F;
                 int nj = INT_MAX;
 #pragma unroll 4

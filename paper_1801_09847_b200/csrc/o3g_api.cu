@@ -132,6 +132,8 @@ struct o3g_ctx {
     int target_sort = 1;  // 0 counting sort, 1 stable radix sort (default: measured faster)
     int prune_min = -1;   // variant 1 row pruning: -1 auto, -2 never, >= 0 threshold
     int interleave = -1;  // variant 1 batch interleave: -1 auto, 0 off, 1 on
+    int xsort = -1;       // target x-order inside cells: -1 auto, 0 off, 1 on
+    bool xsorted = false;
     bool has_normals = false;
 
     // target grid
@@ -151,6 +153,7 @@ struct o3g_ctx {
     bool src_ready = false;
     DevBuf src4;
     DevBuf tiles, tflag;  // variant 4 tile starts (local shard) and scratch
+    DevBuf xk_a, xk_b, xpos, xnrm;   // x-order inside cells (scratch)
     int32_t ntiles = 0;
     // loop
     DevBuf partials, gathered, state, hist_fit, hist_rmse;
@@ -302,7 +305,7 @@ o3g_status o3g_destroy(o3g_ctx* c) {
                       &c->vals_a, &c->vals_b, &c->cub_tmp, &c->stage_a, &c->stage_b, &c->stage_c, &c->misc,
                       &c->src4, &c->partials, &c->gathered, &c->state, &c->hist_fit, &c->hist_rmse,
                       &c->vk_a, &c->vk_b, &c->vflags, &c->vrunid, &c->vstarts, &c->ms_src,
-                      &c->ms_tgt, &c->ms_nrm, &c->ev_T, &c->ev_part, &c->ev_out, &c->tiles, &c->tflag};
+                      &c->ms_tgt, &c->ms_nrm, &c->ev_T, &c->ev_part, &c->ev_out, &c->tiles, &c->tflag, &c->xk_a, &c->xk_b, &c->xpos, &c->xnrm};
     for (DevBuf* b : bufs) b->release();
     if (c->comm && nccl().comm_destroy) nccl().comm_destroy(c->comm);
     if (c->h_state) cudaFreeHost(c->h_state);
@@ -335,6 +338,10 @@ o3g_status o3g_set_option(o3g_ctx* c, int option, int64_t value) {
         case O3G_OPT_TARGET_SORT:
             if (value < 0 || value > 1) return fail(O3G_ERR_INVALID_ARGUMENT, "target sort must be 0 or 1");
             c->target_sort = (int)value;
+            break;
+        case O3G_OPT_XSORT:
+            if (value < -1 || value > 1) return fail(O3G_ERR_INVALID_ARGUMENT, "xsort must be -1, 0 or 1");
+            c->xsort = (int)value;
             break;
         case O3G_OPT_INTERLEAVE:
             if (value < -1 || value > 1) return fail(O3G_ERR_INVALID_ARGUMENT, "interleave must be -1, 0 or 1");
@@ -484,6 +491,34 @@ static o3g_status set_target_impl(o3g_ctx* c, const float* xyz, const float* nor
     c->dmax = dmax;
     c->has_normals = dn != nullptr;
     c->occupied = (int64_t)h_occ;
+    // x-order inside cells for dense targets (the cooperative path's x-windows):
+    // auto when the target averages >= 32 points per occupied cell
+    c->xsorted = false;
+    const bool xs = !g.hashed && (c->xsort == 1 || (c->xsort == -1 && (double)n >= 32.0 * (double)(h_occ ? h_occ : 1)));
+    if (xs) {
+        TRY(c->xk_a.ensure((size_t)n * 8));
+        TRY(c->xk_b.ensure((size_t)n * 8));
+        TRY(c->xpos.ensure((size_t)n * sizeof(float4)));
+        TRY(c->xnrm.ensure((size_t)n * sizeof(float4)));
+        launch_xkeys(c->tpos.as<float4>(), n, g, (uint64_t*)c->xk_a.p, c->vals_a.as<int32_t>(), c->exec);
+        const int eb = 32 + bits_for((uint64_t)(g.table_size - 1));
+        size_t tmp = 0;
+        CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp, (uint64_t*)c->xk_a.p, (uint64_t*)c->xk_b.p,
+                                           c->vals_a.as<int32_t>(), c->vals_b.as<int32_t>(), (int)n, 0, eb,
+                                           c->exec));
+        TRY(c->cub_tmp.ensure(tmp));
+        CK(cub::DeviceRadixSort::SortPairs(c->cub_tmp.p, tmp, (uint64_t*)c->xk_a.p, (uint64_t*)c->xk_b.p,
+                                           c->vals_a.as<int32_t>(), c->vals_b.as<int32_t>(), (int)n, 0, eb,
+                                           c->exec));
+        launch_permute_target(c->tpos.as<float4>(), c->tnrm.as<float4>(), c->vals_b.as<int32_t>(), n,
+                              c->xpos.as<float4>(), c->xnrm.as<float4>(), c->exec);
+        std::swap(c->tpos, c->xpos);
+        std::swap(c->tnrm, c->xnrm);
+        c->launches += 4;
+        CK(cudaStreamSynchronize(c->exec));
+        CK(cudaGetLastError());
+        c->xsorted = true;
+    }
     return O3G_OK;
 }
 
@@ -639,6 +674,7 @@ static K3Args k3_args(o3g_ctx* c, int32_t* corr) {
     // queries cluster in the ordered source and would serialise a few warps)
     const bool ilv = c->interleave == 1 || (c->interleave == -1 && coop_min_of(c) > 0);
     a.ilv = ilv ? (int)((c->n_local + 31) / 32) : 0;
+    a.xsorted = c->xsorted ? 1 : 0;
     a.prune_min = prune_of(c);
     a.prune = a.prune_min >= 0;
     if (!a.prune) a.prune_min = 0;

@@ -88,6 +88,10 @@ void launch_check_finite(const float* v, int64_t count, int32_t* nonfinite, int 
 // needs < 2^10 bricks per axis), 0: the table index
 void launch_cell_keys(const float* xyz, int64_t n, const GridDev& g, const double* T12_or_null,
                       uint32_t* keys, int32_t* vals, cudaStream_t s, int brick = 0);
+void launch_xkeys(const float4* tpos, int64_t n, const GridDev& g, uint64_t* keys, int32_t* vals,
+                  cudaStream_t s);
+void launch_permute_target(const float4* tpos, const float4* tnrm, const int32_t* perm, int64_t n,
+                           float4* opos, float4* onrm, cudaStream_t s);
 void launch_run_marks(const uint32_t* keys, int64_t n, int shift, int32_t* mark, cudaStream_t s);
 void launch_tile_flags(const int32_t* run_start, int64_t n, int tq, uint8_t* flag, cudaStream_t s);
 void launch_histogram(const uint32_t* keys, int64_t n, int32_t* counts, unsigned long long* occupied,
@@ -145,6 +149,7 @@ struct K3Args {
     const int32_t* tiles;      // variant 4: tile starts in the local source (ntiles)
     int32_t ntiles;
     int ilv;                   // variant 1: 0, or interleaved batches (= ceil(n / 32))
+    int xsorted;               // target x-sorted inside cells: x-windows in the cooperative path
     int prune;                 // variant 1: row-pruning instantiation (dense grid)
     int prune_min;             //   ... for light queries with >= prune_min candidates
     // fused tail (single GPU, variant 1): the last block to finish reduces the

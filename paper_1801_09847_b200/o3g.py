@@ -27,7 +27,7 @@ FLAG_NO_CORRESPONDENCES = 1
 FLAG_DEGENERATE = 2
 NTERMS = 29
 (OPT_SEARCH, OPT_GRID, OPT_TIMING, OPT_BLOCKS_PER_SM, OPT_NBR_MASK, OPT_COOP_MIN, OPT_ESTIMATION,
- OPT_SOURCE_ORDER, OPT_TARGET_SORT, OPT_PRUNE_MIN, OPT_INTERLEAVE) = range(1, 12)
+ OPT_SOURCE_ORDER, OPT_TARGET_SORT, OPT_PRUNE_MIN, OPT_INTERLEAVE, OPT_XSORT) = range(1, 13)
 
 
 class O3GError(RuntimeError):

@@ -22,6 +22,8 @@ GOLD = os.path.join(os.path.dirname(__file__), "golden")
 # name -> {option: value}: O3G_OPT_SEARCH (1), O3G_OPT_PRUNE_MIN (10)
 SEARCH = {"exact": {1: 0}, "balanced": {1: 1}, "pruned": {1: 1, 10: 0}, "unpruned": {1: 1, 10: -2},
           "interleaved": {1: 1, 11: 1},
+          # every query cooperative, rows pruned, x-sorted target with x-windows
+          "coopx": {1: 1, 6: 1, 10: 0, 12: 1},
           "prefilter": {1: 2}, "sorted": {1: 3}, "tiled": {1: 4}}
 GRID = {"dense": 1, "hashed": 2}
 

@@ -39,14 +39,25 @@ __global__ void k_bbox(const float* __restrict__ xyz, int64_t n, uint32_t* __res
         }
     }
     bad = __any_sync(0xffffffffu, bad);
+    // block reduce first: 6 atomics per block, not per warp (the per-warp
+    // version serialised ~60k atomics on 6 words: 48 us for 2M points)
+    __shared__ uint32_t s_mm[6];
+    __shared__ int s_bad;
+    if (threadIdx.x < 6) s_mm[threadIdx.x] = threadIdx.x < 3 ? 0xFFFFFFFFu : 0u;
+    if (threadIdx.x == 0) s_bad = 0;
+    __syncthreads();
     if ((threadIdx.x & 31) == 0) {
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
-            atomicMin(&mm[a], f2ord(lo[a]));
-            atomicMax(&mm[3 + a], f2ord(hi[a]));
+            atomicMin(&s_mm[a], f2ord(lo[a]));
+            atomicMax(&s_mm[3 + a], f2ord(hi[a]));
         }
-        if (bad) atomicOr(nonfinite, 1);
+        if (bad) s_bad = 1;
     }
+    __syncthreads();
+    if (threadIdx.x < 3) atomicMin(&mm[threadIdx.x], s_mm[threadIdx.x]);
+    else if (threadIdx.x < 6) atomicMax(&mm[threadIdx.x], s_mm[threadIdx.x]);
+    if (threadIdx.x == 0 && s_bad) atomicOr(nonfinite, 1);
 }
 
 __global__ void k_check_finite(const float* __restrict__ v, int64_t count, int32_t* nonfinite) {

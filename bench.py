@@ -50,6 +50,7 @@ def parse():
     ap.add_argument("--prune-min", type=int, default=None, help="override O3G_OPT_PRUNE_MIN")
     ap.add_argument("--interleave", type=int, default=None, help="override O3G_OPT_INTERLEAVE")
     ap.add_argument("--xsort", type=int, default=None, help="override O3G_OPT_XSORT")
+    ap.add_argument("--nbr-mask", type=int, default=None, help="override O3G_OPT_NBR_MASK")
     ap.add_argument("--regime", default="init", choices=["init", "converged"],
                     help="start from the config's init T (default) or from T* perturbed by 0.1 deg / 1 cm "
                          "(SURVEY 8(d) 'converged-regime' run)")
@@ -226,6 +227,8 @@ def main():
         ctx.set_option(11, a.interleave)
     if a.xsort is not None:
         ctx.set_option(12, a.xsort)
+    if a.nbr_mask is not None:
+        ctx.set_option(5, a.nbr_mask)
     if a.bps is not None:
         ctx.set_option(4, a.bps)
     if world > 1:

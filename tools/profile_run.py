@@ -18,6 +18,7 @@ ap.add_argument("--bps", type=int, default=0)
 ap.add_argument("--coop-min", type=int, default=None)
 ap.add_argument("--prune-min", type=int, default=None)
 ap.add_argument("--interleave", type=int, default=None)
+ap.add_argument("--regime", default="init", choices=["init", "converged"])
 a = ap.parse_args()
 
 import torch  # noqa: E402
@@ -26,6 +27,13 @@ import paper_1801_09847_b200 as o3g  # noqa: E402
 from bench import load_workload  # noqa: E402
 
 w = load_workload(a.config, a.n)
+if a.regime == "converged":   # as bench.py --regime converged
+    import numpy as np
+    from synth.rng import Stream
+    from synth.scenes import rigid, rotation
+    rs = Stream(0x5EED)
+    w = dict(w, init_T=w["T_true"] @ rigid(rotation(rs.unit_vectors(1)[0], np.deg2rad(0.1)),
+                                             0.01 * rs.unit_vectors(1)[0]))
 dev = torch.device("cuda:0")
 src, tgt, nrm = (torch.from_numpy(w[k]).to(dev) for k in ("source", "target", "target_normals"))
 ctx = o3g.Context(0)

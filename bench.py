@@ -51,6 +51,7 @@ def parse():
     ap.add_argument("--interleave", type=int, default=None, help="override O3G_OPT_INTERLEAVE")
     ap.add_argument("--xsort", type=int, default=None, help="override O3G_OPT_XSORT")
     ap.add_argument("--nbr-mask", type=int, default=None, help="override O3G_OPT_NBR_MASK")
+    ap.add_argument("--grid", type=int, default=None, help="override O3G_OPT_GRID (1 dense, 2 hashed)")
     ap.add_argument("--regime", default="init", choices=["init", "converged"],
                     help="start from the config's init T (default) or from T* perturbed by 0.1 deg / 1 cm "
                          "(SURVEY 8(d) 'converged-regime' run)")
@@ -229,6 +230,8 @@ def main():
         ctx.set_option(12, a.xsort)
     if a.nbr_mask is not None:
         ctx.set_option(5, a.nbr_mask)
+    if a.grid is not None:
+        ctx.set_option(2, a.grid)
     if a.bps is not None:
         ctx.set_option(4, a.bps)
     if world > 1:

@@ -297,6 +297,13 @@ def main():
         ms = float(t.item())
     value = units / (ms / 1e3)
 
+    # per-pass fitness of one (untimed) registration (SURVEY 8(d) config-5 caveat)
+    hist_fit = None
+    if not multiscale:
+        ctx.set_target(tgt, nrm, w["dmax"])
+        ctx.set_source(src, T0)
+        hist_fit = [round(float(f), 6) for f in ctx.run(T0, iters, 0.0, 0.0, history=True).hist_fitness]
+
     # dominant kernel (K3) live duration with CUDA events inside the run graph
     ctx.set_option(o3g.o3g.OPT_TIMING, 1)
     t_loop = []
@@ -398,7 +405,8 @@ def main():
                        "k3_total_ms": k3_ms, "tail_total_ms": tail_ms, "k3_launches": k3_n,
                        "fitness": (float(res["fitness"][-1]) if multiscale else res.fitness),
                        "inlier_rmse": (float(res["inlier_rmse"][-1]) if multiscale else res.inlier_rmse),
-                       "grid": ctx.grid_info()},
+                       "grid": ctx.grid_info(),
+                       "hist_fitness": hist_fit},
         }
         print(json.dumps(out), flush=True)
     ctx.close()

@@ -147,6 +147,7 @@ struct o3g_ctx {
     DevBuf keys_a, keys_b, vals_a, vals_b, cub_tmp, stage_a, stage_b, stage_c, misc;
     // voxel_down_sample / multi-scale scratch
     DevBuf vk_a, vk_b, vflags, vrunid, vstarts, ms_src, ms_tgt, ms_nrm;
+    DevBuf ms_in_src, ms_in_tgt, ms_in_nrm;   // multi-scale: host inputs copied once
     DevBuf ev_T, ev_part, ev_out;
     // source
     int64_t n_total = 0, n_local = 0, shard_lo = 0;
@@ -305,7 +306,7 @@ o3g_status o3g_destroy(o3g_ctx* c) {
                       &c->vals_a, &c->vals_b, &c->cub_tmp, &c->stage_a, &c->stage_b, &c->stage_c, &c->misc,
                       &c->src4, &c->partials, &c->gathered, &c->state, &c->hist_fit, &c->hist_rmse,
                       &c->vk_a, &c->vk_b, &c->vflags, &c->vrunid, &c->vstarts, &c->ms_src,
-                      &c->ms_tgt, &c->ms_nrm, &c->ev_T, &c->ev_part, &c->ev_out, &c->tiles, &c->tflag, &c->xk_a, &c->xk_b, &c->xpos, &c->xnrm};
+                      &c->ms_tgt, &c->ms_nrm, &c->ev_T, &c->ev_part, &c->ev_out, &c->tiles, &c->tflag, &c->ms_in_src, &c->ms_in_tgt, &c->ms_in_nrm, &c->xk_a, &c->xk_b, &c->xpos, &c->xnrm};
     for (DevBuf* b : bufs) b->release();
     if (c->comm && nccl().comm_destroy) nccl().comm_destroy(c->comm);
     if (c->h_state) cudaFreeHost(c->h_state);
@@ -1094,12 +1095,38 @@ extern "C" o3g_status o3g_icp_multiscale(o3g_ctx* c, const float* src, int64_t n
     TRY(c->ms_src.ensure((size_t)n * 12));
     TRY(c->ms_tgt.ensure((size_t)m * 12));
     TRY(c->ms_nrm.ensure((size_t)m * 12));
+    // host inputs: copied to the device once (not once per scale), on the copy
+    // stream, target first, so the first target downsample overlaps the source copy
+    const bool host = !is_device_ptr(src) || !is_device_ptr(tgt) || !is_device_ptr(nrm);
+    if (host) {
+        CK(cudaSetDevice(c->device));
+        if (!c->copy) {
+            CK(cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking));
+            for (cudaEvent_t& e : c->ev_copy) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        }
+        TRY(c->ms_in_src.ensure((size_t)n * 12));
+        TRY(c->ms_in_tgt.ensure((size_t)m * 12));
+        TRY(c->ms_in_nrm.ensure((size_t)m * 12));
+        TRY(enter(c));
+        CK(cudaEventRecord(c->ev_copy[3], c->exec));
+        CK(cudaStreamWaitEvent(c->copy, c->ev_copy[3], 0));
+        CK(cudaMemcpyAsync(c->ms_in_tgt.p, tgt, (size_t)m * 12, cudaMemcpyDefault, c->copy));
+        CK(cudaMemcpyAsync(c->ms_in_nrm.p, nrm, (size_t)m * 12, cudaMemcpyDefault, c->copy));
+        CK(cudaEventRecord(c->ev_copy[0], c->copy));
+        CK(cudaMemcpyAsync(c->ms_in_src.p, src, (size_t)n * 12, cudaMemcpyDefault, c->copy));
+        CK(cudaEventRecord(c->ev_copy[2], c->copy));
+        CK(cudaStreamWaitEvent(c->exec, c->ev_copy[0], 0));
+        src = c->ms_in_src.as<float>();
+        tgt = c->ms_in_tgt.as<float>();
+        nrm = c->ms_in_nrm.as<float>();
+    }
     double T[16];
     memcpy(T, init_T, sizeof(T));
     for (int s = 0; s < ns; ++s) {
         int64_t nsrc = 0, ntgt = 0;
         TRY(voxel_impl(c, tgt, nrm, m, voxel[s], c->ms_tgt.as<float>(), c->ms_nrm.as<float>(), &ntgt));
         TRY(o3g_set_target(c, c->ms_tgt.as<float>(), c->ms_nrm.as<float>(), ntgt, dmax[s]));
+        if (host && s == 0) CK(cudaStreamWaitEvent(c->exec, c->ev_copy[2], 0));
         TRY(voxel_impl(c, src, nullptr, n, voxel[s], c->ms_src.as<float>(), nullptr, &nsrc));
         TRY(o3g_set_source(c, c->ms_src.as<float>(), nsrc, T));
         double fit = 0, rmse = 0, Tn[16];

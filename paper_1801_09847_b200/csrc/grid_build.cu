@@ -110,6 +110,21 @@ __global__ void k_cell_keys(const float* __restrict__ xyz, int64_t n, GridDev g,
     }
 }
 
+// hashed grid: occupancy of coarse cells (2^shift fine cells per axis), the
+// live-query test's structure when no dense per-cell bitmap fits
+__global__ void k_coarse_bits(const float4* __restrict__ tpos, int64_t n, GridDev g, int shift, int cnx, int cny,
+                              uint32_t* __restrict__ bits) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const float4 p = tpos[i];
+        const int cx = min(max(cell_coord((double)p.x, g.ox, g.inv_h, g.nx), 0), g.nx - 1) >> shift;
+        const int cy = min(max(cell_coord((double)p.y, g.oy, g.inv_h, g.ny), 0), g.ny - 1) >> shift;
+        const int cz = min(max(cell_coord((double)p.z, g.oz, g.inv_h, g.nz), 0), g.nz - 1) >> shift;
+        const int64_t k = ((int64_t)cz * cny + cy) * cnx + cx;
+        atomicOr(&bits[k >> 5], 1u << (k & 31));
+    }
+}
+
 // x-order inside cells (O3G_OPT_XSORT): key = cell << 32 | order-preserving
 // bits of x, value = current position; then the target is permuted
 __global__ void k_xkeys(const float4* __restrict__ tpos, int64_t n, GridDev g, uint64_t* __restrict__ keys,
@@ -267,6 +282,10 @@ void launch_cell_keys(const float* xyz, int64_t n, const GridDev& g, const doubl
                                                    t[4], t[5], t[6], t[7], t[8], t[9], t[10], t[11],
                                                    keys, vals, brick);
 }
+void launch_coarse_bits(const float4* tpos, int64_t n, const GridDev& g, int shift, int cnx, int cny,
+                        uint32_t* bits, cudaStream_t s) {
+    k_coarse_bits<<<blocks_for(n, 256), 256, 0, s>>>(tpos, n, g, shift, cnx, cny, bits);
+}
 void launch_xkeys(const float4* tpos, int64_t n, const GridDev& g, uint64_t* keys, int32_t* vals,
                   cudaStream_t s) {
     k_xkeys<<<blocks_for(n, 256), 256, 0, s>>>(tpos, n, g, keys, vals);
@@ -297,6 +316,13 @@ void launch_gather_target(const float* xyz, const float* nrm, const int32_t* val
 void launch_gather_source(const float* xyz, const int32_t* vals, int64_t lo, int64_t hi,
                           float4* out, cudaStream_t s) {
     k_gather_source<<<blocks_for(hi - lo, 256), 256, 0, s>>>(xyz, vals, lo, hi, out);
+}
+void launch_dilate3(uint32_t* bits, uint32_t* tmp, int64_t ncells, int64_t nx, int64_t nxny, cudaStream_t s) {
+    const int64_t nw = (ncells + 31) / 32;
+    k_dilate_bits<<<blocks_for(nw, 256), 256, 0, s>>>(bits, tmp, nw, 1);
+    k_dilate_bits<<<blocks_for(nw, 256), 256, 0, s>>>(tmp, bits, nw, nx);
+    k_dilate_bits<<<blocks_for(nw, 256), 256, 0, s>>>(bits, tmp, nw, nxny);
+    cudaMemcpyAsync(bits, tmp, nw * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s);
 }
 void launch_nbr_bits(const int32_t* cs, int64_t ncells, int64_t nx, int64_t nxny, uint32_t* tmp,
                      uint32_t* out, cudaStream_t s) {

@@ -229,6 +229,24 @@ __device__ __forceinline__ int warp_bound_x(const float4* __restrict__ tpos, int
 __device__ __noinline__ void tail_finish(const double* terms, IcpState* st, double* hist_fit, double* hist_rmse,
                             int mode);
 
+// live test of the query in cell (cx, cy, cz) (cells in [-2, n+1]): one bit
+// of the dilated occupancy bitmap — per cell on a dense grid; on a hashed grid
+// per 2^cshift-cell coarse cell (the fine stencil [c-1, c+1] lies inside the
+// coarse cells [C-1, C+1], C = c >> cshift, which the dilation covers).
+// Conservative: a false positive only costs a full search.
+__device__ __forceinline__ bool stencil_live(const K3Args& a, const GridDev& g, int cx, int cy, int cz) {
+    if (cx < -1 || cx > g.nx || cy < -1 || cy > g.ny || cz < -1 || cz > g.nz) return false;
+    if (!g.hashed) {   // (dense: table_size < 2^31, 32-bit index)
+        const int kc = (min(max(cz, 0), g.nz - 1) * g.ny + min(max(cy, 0), g.ny - 1)) * g.nx +
+                       min(max(cx, 0), g.nx - 1);
+        return (__ldg(&a.nbr_bits[kc >> 5]) >> (kc & 31)) & 1u;
+    }
+    const int s = a.cshift;
+    const int64_t k = ((int64_t)(min(max(cz, 0), g.nz - 1) >> s) * a.cny + (min(max(cy, 0), g.ny - 1) >> s)) * a.cnx +
+                      (min(max(cx, 0), g.nx - 1) >> s);
+    return (__ldg(&a.nbr_bits[k >> 5]) >> (k & 31)) & 1u;
+}
+
 template <bool WRITE_CORR, bool COOP, bool PRUNE>
 __global__ void __launch_bounds__(kK3Threads, 4) k3_balanced(const K3Args a) {
     extern __shared__ __align__(16) unsigned char k3smem[];
@@ -284,10 +302,14 @@ __global__ void __launch_bounds__(kK3Threads, 4) k3_balanced(const K3Args a) {
                 const int cx = cell_coord(tx, g.ox, g.inv_h, g.nx);
                 const int cy = cell_coord(ty, g.oy, g.inv_h, g.ny);
                 const int cz = cell_coord(tz, g.oz, g.inv_h, g.nz);
-                if (cx >= -1 && cx <= g.nx && cy >= -1 && cy <= g.ny && cz >= -1 && cz <= g.nz) {
-                    const int kc = (min(max(cz, 0), g.nz - 1) * g.ny + min(max(cy, 0), g.ny - 1)) * g.nx +
-                                   min(max(cx, 0), g.nx - 1);
-                    live = (__ldg(&a.nbr_bits[kc >> 5]) >> (kc & 31)) & 1u;
+                if (!g.hashed) {
+                    if (cx >= -1 && cx <= g.nx && cy >= -1 && cy <= g.ny && cz >= -1 && cz <= g.nz) {
+                        const int kc = (min(max(cz, 0), g.nz - 1) * g.ny + min(max(cy, 0), g.ny - 1)) * g.nx +
+                                       min(max(cx, 0), g.nx - 1);
+                        live = (__ldg(&a.nbr_bits[kc >> 5]) >> (kc & 31)) & 1u;
+                    }
+                } else {
+                    live = stencil_live(a, g, cx, cy, cz);
                 }
                 if (WRITE_CORR && !live) a.corr_out[__float_as_int(p0.w)] = -1;
             }
@@ -330,11 +352,14 @@ __global__ void __launch_bounds__(kK3Threads, 4) k3_balanced(const K3Args a) {
             const int ylo = max(cy - 1, 0), yhi = min(cy + 1, g.ny - 1);
             const int zlo = max(cz - 1, 0), zhi = min(cz + 1, g.nz - 1);
             bool near = xlo <= xhi && ylo <= yhi && zlo <= zhi;
-            if (near && a.nbr_bits) {
-                // dilated occupancy bitmap: skip queries with no occupied neighbour cell
-                const int kc = (min(max(cz, 0), g.nz - 1) * g.ny + min(max(cy, 0), g.ny - 1)) * g.nx +
-                               min(max(cx, 0), g.nx - 1);
-                near = (__ldg(&a.nbr_bits[kc >> 5]) >> (kc & 31)) & 1u;
+            if (near && a.nbr_bits) {   // skip queries with no occupied stencil cell
+                if (!g.hashed) {
+                    const int kc = (min(max(cz, 0), g.nz - 1) * g.ny + min(max(cy, 0), g.ny - 1)) * g.nx +
+                                   min(max(cx, 0), g.nx - 1);
+                    near = (__ldg(&a.nbr_bits[kc >> 5]) >> (kc & 31)) & 1u;
+                } else {
+                    near = stencil_live(a, g, cx, cy, cz);
+                }
             }
             if (!g.hashed && near) {
                 // dense table: all 18 row-boundary loads issued back to back;

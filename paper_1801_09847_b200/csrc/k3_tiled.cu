@@ -110,7 +110,7 @@ __global__ void __launch_bounds__(kTT, 6) k3_tiled(const K3Args a) {
                 if (cx >= -1 && cx <= g.nx && cy >= -1 && cy <= g.ny && cz >= -1 && cz <= g.nz) {
                     const int kc = (min(max(cz, 0), g.nz - 1) * g.ny + min(max(cy, 0), g.ny - 1)) * g.nx +
                                    min(max(cx, 0), g.nx - 1);
-                    live = a.nbr_bits ? ((__ldg(&a.nbr_bits[kc >> 5]) >> (kc & 31)) & 1u) : true;
+                    live = a.nbr_bits && !g.hashed ? ((__ldg(&a.nbr_bits[kc >> 5]) >> (kc & 31)) & 1u) : true;
                 }
                 if (WRITE_CORR && !live) a.corr_out[__float_as_int(p.w)] = -1;
             }

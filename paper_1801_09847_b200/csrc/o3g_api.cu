@@ -143,6 +143,7 @@ struct o3g_ctx {
     int64_t occupied = 0;
     DevBuf tpos, tnrm, cell_start, counts, nbr_a, nbr_b;
     bool nbr_ready = false;
+    int cshift = 0, cnx = 0, cny = 0;   // hashed grid: coarse occupancy bitmap (nbr_a)
     // scratch
     DevBuf keys_a, keys_b, vals_a, vals_b, cub_tmp, stage_a, stage_b, stage_c, misc;
     // voxel_down_sample / multi-scale scratch
@@ -479,6 +480,25 @@ static o3g_status set_target_impl(o3g_ctx* c, const float* xyz, const float* nor
                         c->nbr_b.as<uint32_t>(), c->nbr_a.as<uint32_t>(), c->exec);
         c->launches += 4;
         c->nbr_ready = true;
+    } else {
+        // hashed grid: coarse occupancy bitmap (<= 2^30 bits) for the live test
+        int sh = 0;
+        while ((double)(((int64_t)g.nx + (1 << sh) - 1) >> sh) * (double)(((int64_t)g.ny + (1 << sh) - 1) >> sh) *
+                   (double)(((int64_t)g.nz + (1 << sh) - 1) >> sh) > 1073741824.0)
+            ++sh;
+        c->cshift = sh;
+        c->cnx = (int)(((int64_t)g.nx + (1 << sh) - 1) >> sh);
+        c->cny = (int)(((int64_t)g.ny + (1 << sh) - 1) >> sh);
+        const int64_t cnz = ((int64_t)g.nz + (1 << sh) - 1) >> sh;
+        const int64_t ncc = (int64_t)c->cnx * c->cny * cnz, nw = (ncc + 31) / 32;
+        TRY(c->nbr_a.ensure(nw * 4));
+        TRY(c->nbr_b.ensure(nw * 4));
+        CK(cudaMemsetAsync(c->nbr_a.p, 0, nw * 4, c->exec));
+        launch_coarse_bits(c->tpos.as<float4>(), n, g, sh, c->cnx, c->cny, c->nbr_a.as<uint32_t>(), c->exec);
+        launch_dilate3(c->nbr_a.as<uint32_t>(), c->nbr_b.as<uint32_t>(), ncc, c->cnx, (int64_t)c->cnx * c->cny,
+                       c->exec);
+        c->launches += 4;
+        c->nbr_ready = true;
     }
     unsigned long long h_occ = 0;
     int32_t h_bad2 = 0;
@@ -665,6 +685,7 @@ static K3Args k3_args(o3g_ctx* c, int32_t* corr) {
     a.block_partials = c->partials.as<double>();
     a.corr_out = corr;
     a.nbr_bits = (c->nbr_mask && c->nbr_ready) ? c->nbr_a.as<uint32_t>() : nullptr;
+    a.cshift = c->cshift, a.cnx = c->cnx, a.cny = c->cny;
     a.p2p = c->estimation;
     a.eval_T = nullptr;
     a.n_eval = 0;

@@ -88,6 +88,9 @@ void launch_check_finite(const float* v, int64_t count, int32_t* nonfinite, int 
 // needs < 2^10 bricks per axis), 0: the table index
 void launch_cell_keys(const float* xyz, int64_t n, const GridDev& g, const double* T12_or_null,
                       uint32_t* keys, int32_t* vals, cudaStream_t s, int brick = 0);
+void launch_dilate3(uint32_t* bits, uint32_t* tmp, int64_t ncells, int64_t nx, int64_t nxny, cudaStream_t s);
+void launch_coarse_bits(const float4* tpos, int64_t n, const GridDev& g, int shift, int cnx, int cny,
+                        uint32_t* bits, cudaStream_t s);
 void launch_xkeys(const float4* tpos, int64_t n, const GridDev& g, uint64_t* keys, int32_t* vals,
                   cudaStream_t s);
 void launch_permute_target(const float4* tpos, const float4* tnrm, const int32_t* perm, int64_t n,
@@ -139,7 +142,9 @@ struct K3Args {
     double* block_partials; // [gridDim.x][kTermStride]
     int32_t* corr_out;      // original order, nullable
     const uint32_t* nbr_bits;  // dense grid: bit k set iff some cell of k's 27-stencil
-                               // is occupied (a conservative skip test); nullable
+                               // is occupied (a conservative skip test); hashed grid:
+                               // the same over 2^cshift-cell coarse cells; nullable
+    int cshift, cnx, cny;      // hashed grid: coarse cell = cell >> cshift, dims
     int p2p;                   // record = point-to-point terms (sum s'q^T, sum s', sum q)
     int n_eval;
     const double* eval_T;      // batched evaluation: T of blockIdx.y is eval_T[16 * y]

@@ -279,6 +279,7 @@ __global__ void __launch_bounds__(kK3Threads, 4) k3_balanced(const K3Args a) {
     // vs 0.733 ms at T_init, 1.145 vs 1.039 ms converged). Results are the
     // same either way.
     const bool use_queue = a.nbr_bits != nullptr && !(!a.eval_T && a.st->passes > 0 && a.st->fit > 0.7);
+    const bool warm = !PRUNE && a.prev_j && !a.eval_T && a.st->passes > 0;
     __shared__ float4 s_gap[PRUNE && COOP ? kK3Threads / 32 : 1][32];
     __shared__ int s_rmask[PRUNE && COOP ? kK3Threads / 32 : 1][32];
     int qn = 0;   // warp-uniform queue length
@@ -312,6 +313,7 @@ __global__ void __launch_bounds__(kK3Threads, 4) k3_balanced(const K3Args a) {
                     live = stencil_live(a, g, cx, cy, cz);
                 }
                 if (WRITE_CORR && !live) a.corr_out[__float_as_int(p0.w)] = -1;
+                if (!PRUNE && a.prev_j && !live) a.prev_j[i0] = -1;   // (no winner: no warm start)
             }
             const unsigned lb = __ballot_sync(0xffffffffu, live);
             if (live) qbuf[warp][qn + __popc(lb & ((1u << lane) - 1u))] = i0;
@@ -376,9 +378,30 @@ __global__ void __launch_bounds__(kK3Threads, 4) k3_balanced(const K3Args a) {
                     ee[r] = ok ? __ldg(cs + rb + w) : 0;
                 }
                 if (!PRUNE) {
+                    // warm start (the loop's passes after the first): the fp64 d2
+                    // of the previous pass's winner bounds this pass's winner, so
+                    // rows with L > that bound are not staged (§5.2c; a
+                    // neighbour within r lies in the stencil, §5.1, so the bound
+                    // is either attained in the stencil or above r^2)
+                    float ub = CUDART_INF_F;
+                    float gym = 0.f, gyp = 0.f, gzm = 0.f, gzp = 0.f;
+                    if (warm) {
+                        const int jp = __ldg(&a.prev_j[i]);
+                        if (jp >= 0) {
+                            const float4 t = __ldg(&a.tpos[jp]);
+                            const double dx = __dsub_rn(sx, (double)t.x), dy = __dsub_rn(sy, (double)t.y),
+                                         dz = __dsub_rn(sz, (double)t.z);
+                            const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)),
+                                                        __dmul_rn(dz, dz));
+                            ub = __double2float_ru(d2 * (1.0 + 9.094947017729282e-13));   // (1 + 2^-40), up
+                            face_gaps(sy, g.oy, g.h, cy, gym, gyp);
+                            face_gaps(sz, g.oz, g.h, cz, gzm, gzp);
+                        }
+                    }
 #pragma unroll
                     for (int r = 0; r < 9; ++r) {
-                        if (ee[r] > bb[r]) {
+                        if (ee[r] > bb[r] &&
+                            (r == 4 || !(row_lower(r % 3 - 1, r / 3 - 1, gym, gyp, gzm, gzp) > ub))) {
                             segs[nseg * 32 + lane] = make_int2(bb[r], ee[r]);
                             ++nseg;
                             c += ee[r] - bb[r];
@@ -701,6 +724,7 @@ __global__ void __launch_bounds__(kK3Threads, 4) k3_balanced(const K3Args a) {
             }
         }
         if (WRITE_CORR && i < a.n) a.corr_out[__float_as_int(p.w)] = widx;
+        if (!PRUNE && a.prev_j && i < a.n) a.prev_j[i] = win;   // the next pass's warm start
 
         // A5: r = (s'-q).n, J = [s' x n ; n] (R4) -> V = (J, r, m), W = (J, m, d2)
         const unsigned matched = __ballot_sync(0xffffffffu, win >= 0);

@@ -154,6 +154,8 @@ struct o3g_ctx {
     int64_t n_total = 0, n_local = 0, shard_lo = 0;
     bool src_ready = false;
     DevBuf src4;
+    DevBuf prevj;          // run loop: previous pass's winner per local query
+    const void* gkey_prev = nullptr;
     DevBuf tiles, tflag;  // variant 4 tile starts (local shard) and scratch
     DevBuf xk_a, xk_b, xpos, xnrm;   // x-order inside cells (scratch)
     int32_t ntiles = 0;
@@ -307,7 +309,7 @@ o3g_status o3g_destroy(o3g_ctx* c) {
                       &c->vals_a, &c->vals_b, &c->cub_tmp, &c->stage_a, &c->stage_b, &c->stage_c, &c->misc,
                       &c->src4, &c->partials, &c->gathered, &c->state, &c->hist_fit, &c->hist_rmse,
                       &c->vk_a, &c->vk_b, &c->vflags, &c->vrunid, &c->vstarts, &c->ms_src,
-                      &c->ms_tgt, &c->ms_nrm, &c->ev_T, &c->ev_part, &c->ev_out, &c->tiles, &c->tflag, &c->ms_in_src, &c->ms_in_tgt, &c->ms_in_nrm, &c->xk_a, &c->xk_b, &c->xpos, &c->xnrm};
+                      &c->ms_tgt, &c->ms_nrm, &c->ev_T, &c->ev_part, &c->ev_out, &c->tiles, &c->tflag, &c->prevj, &c->ms_in_src, &c->ms_in_tgt, &c->ms_in_nrm, &c->xk_a, &c->xk_b, &c->xpos, &c->xnrm};
     for (DevBuf* b : bufs) b->release();
     if (c->comm && nccl().comm_destroy) nccl().comm_destroy(c->comm);
     if (c->h_state) cudaFreeHost(c->h_state);
@@ -697,6 +699,7 @@ static K3Args k3_args(o3g_ctx* c, int32_t* corr) {
     const bool ilv = c->interleave == 1 || (c->interleave == -1 && coop_min_of(c) > 0);
     a.ilv = ilv ? (int)((c->n_local + 31) / 32) : 0;
     a.xsorted = c->xsorted ? 1 : 0;
+    a.prev_j = nullptr;   // (set by the run loop: o3g_icp_run)
     a.prune_min = prune_of(c);
     a.prune = a.prune_min >= 0;
     if (!a.prune) a.prune_min = 0;
@@ -709,12 +712,14 @@ static K3Args k3_args(o3g_ctx* c, int32_t* corr) {
 
 // One pass: K3, then the tail (with the rank exchange when distributed).
 static o3g_status enqueue_pass(o3g_ctx* c, int blocks, bool write_corr, int32_t* corr,
-                               int tail_mode, cudaEvent_t ev0, cudaEvent_t ev1, int* nlaunch) {
+                               int tail_mode, cudaEvent_t ev0, cudaEvent_t ev1, int* nlaunch,
+                               int32_t* prev_j = nullptr) {
     if (ev0) CK(cudaEventRecordWithFlags(ev0, c->exec, cudaEventRecordExternal));
     const bool fused = c->world == 1 && k3_variant(c) == 1 && c->n_local > 0;
     if (c->estimation) tail_mode |= TAIL_P2P;
     if (c->n_local > 0) {
         K3Args ka = k3_args(c, corr);
+        ka.prev_j = prev_j;
         if (fused) {
             ka.fuse_mode = tail_mode;
             ka.counter = c->misc.as<unsigned int>() + 12;   // see set_target's misc layout
@@ -808,8 +813,10 @@ static o3g_status build_graph(o3g_ctx* c, int max_it, int blocks) {
     const void* ptrs[8] = {c->src4.p, c->tpos.p, c->tnrm.p, c->cell_start.p, c->partials.p,
                            c->state.p, c->hist_fit.p, c->gathered.p};
     memcpy(key.ptrs, ptrs, sizeof(ptrs));
-    if (c->gexec && c->gkey == key) return O3G_OK;
+    if (c->gexec && c->gkey == key && c->gkey_prev == c->prevj.p) return O3G_OK;
     invalidate_graph(c);
+    // warm-start buffer: each pass records its winners for the next one
+    TRY(c->prevj.ensure((size_t)(c->n_local > 0 ? c->n_local : 1) * 4));
     const size_t nev = c->timing ? 2 * (size_t)(max_it + 1) : 0;
     while (c->events.size() < nev) {
         cudaEvent_t ev;
@@ -817,12 +824,14 @@ static o3g_status build_graph(o3g_ctx* c, int max_it, int blocks) {
         c->events.push_back(ev);
     }
     CK(cudaStreamBeginCapture(c->exec, cudaStreamCaptureModeThreadLocal));
+    // the first pass has no previous winners: every entry starts at -1
+    if (c->n_local > 0) CK(cudaMemsetAsync(c->prevj.p, 0xFF, (size_t)c->n_local * 4, c->exec));
     int nl = 0;
     o3g_status st = O3G_OK;
     for (int p = 0; p <= max_it && st == O3G_OK; ++p)
         st = enqueue_pass(c, blocks, false, nullptr, TAIL_SOLVE,
                           c->timing ? c->events[2 * p] : nullptr,
-                          c->timing ? c->events[2 * p + 1] : nullptr, &nl);
+                          c->timing ? c->events[2 * p + 1] : nullptr, &nl, c->prevj.as<int32_t>());
     cudaGraph_t graph = nullptr;
     cudaError_t e = cudaStreamEndCapture(c->exec, &graph);
     if (st != O3G_OK) {
@@ -841,6 +850,7 @@ static o3g_status build_graph(o3g_ctx* c, int max_it, int blocks) {
         return fail(O3G_ERR_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
     }
     c->gkey = key;
+    c->gkey_prev = c->prevj.p;
     c->graph_launches = nl;
     return O3G_OK;
 }

@@ -154,6 +154,8 @@ struct K3Args {
     const int32_t* tiles;      // variant 4: tile starts in the local source (ntiles)
     int32_t ntiles;
     int ilv;                   // variant 1: 0, or interleaved batches (= ceil(n / 32))
+    int32_t* prev_j;           // variant 1 run loop: per local query, the previous pass's
+                               // winner (sorted target position, -1 none); nullable
     int xsorted;               // target x-sorted inside cells: x-windows in the cooperative path
     int prune;                 // variant 1: row-pruning instantiation (dense grid)
     int prune_min;             //   ... for light queries with >= prune_min candidates

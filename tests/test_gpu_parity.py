@@ -484,3 +484,20 @@ def test_one_shot_overlapped_host_inputs(o3g, workloads):
     c = o3g.icp_point_to_plane(w["source"], w["target"], w["target_normals"], w["dmax"],
                                w["init_T"], w["iters"])
     assert np.array_equal(c.transformation, b.transformation)
+
+
+def test_loop_parity_warm_start(o3g, workloads):
+    """The run loop's warm start (rows pruned by the previous pass's winner,
+    DESIGN.md §5.2c) on a sparse 400k-point scene where queries move between
+    dead and live across passes: same loop as the oracle."""
+    w = workloads("large16m", n=400_000)
+    T0 = w["T_true"] @ _perturb(31, 0.004, 0.01)
+    ref = oracle.icp(w["source"], w["target"], w["target_normals"], w["dmax"], 6, init_T=T0)
+    for search in ("balanced", "unpruned"):
+        with _ctx(o3g, w, search, order_T=T0) as ctx:
+            r = ctx.run(T0, 6, history=True)
+        assert np.abs(r.transformation - ref["T"]).max() <= 1e-6, search
+        assert abs(r.fitness - ref["fitness"]) <= 1e-6 and abs(r.inlier_rmse - ref["inlier_rmse"]) <= 1e-6
+        assert r.iterations == ref["iterations"]
+        n = min(len(r.hist_fitness), len(ref["hist_fitness"]))
+        assert np.abs(r.hist_fitness[:n] - ref["hist_fitness"][:n]).max() <= 1e-6

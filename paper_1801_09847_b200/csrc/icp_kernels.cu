@@ -279,9 +279,10 @@ __global__ void __launch_bounds__(kK3Threads, 4) k3_balanced(const K3Args a) {
     // vs 0.733 ms at T_init, 1.145 vs 1.039 ms converged). Results are the
     // same either way.
     const bool use_queue = a.nbr_bits != nullptr && !(!a.eval_T && a.st->passes > 0 && a.st->fit > 0.7);
-    const bool warm = !PRUNE && a.prev_j && !a.eval_T && a.st->passes > 0;
+    const bool warm = a.prev_j && !a.eval_T && a.st->passes > 0;
     __shared__ float4 s_gap[PRUNE && COOP ? kK3Threads / 32 : 1][32];
     __shared__ int s_rmask[PRUNE && COOP ? kK3Threads / 32 : 1][32];
+    __shared__ float s_uw[PRUNE && COOP ? kK3Threads / 32 : 1][32];   // warm bound per query
     int qn = 0;   // warp-uniform queue length
     int base = gw * 32;
     for (;;) {
@@ -313,7 +314,7 @@ __global__ void __launch_bounds__(kK3Threads, 4) k3_balanced(const K3Args a) {
                     live = stencil_live(a, g, cx, cy, cz);
                 }
                 if (WRITE_CORR && !live) a.corr_out[__float_as_int(p0.w)] = -1;
-                if (!PRUNE && a.prev_j && !live) a.prev_j[i0] = -1;   // (no winner: no warm start)
+                if (a.prev_j && !live) a.prev_j[i0] = -1;   // (no winner: no warm start)
             }
             const unsigned lb = __ballot_sync(0xffffffffu, live);
             if (live) qbuf[warp][qn + __popc(lb & ((1u << lane) - 1u))] = i0;
@@ -425,12 +426,28 @@ __global__ void __launch_bounds__(kK3Threads, 4) k3_balanced(const K3Args a) {
                         if (ee[r] > bb[r]) fb = bb[r], fe = ee[r];
                     }
                     float ub = CUDART_INF_F;
-                    if (tot >= a.prune_min || (COOP && tot >= a.coop_min)) {
+                    // warm start (passes after the first): the previous winner's
+                    // fp64 d2 bounds this pass's winner (see the plain path)
+                    float uw = CUDART_INF_F;
+                    if (warm) {
+                        const int jp = __ldg(&a.prev_j[i]);
+                        if (jp >= 0) {
+                            const float4 t = __ldg(&a.tpos[jp]);
+                            const double dx = __dsub_rn(sx, (double)t.x), dy = __dsub_rn(sy, (double)t.y),
+                                         dz = __dsub_rn(sz, (double)t.z);
+                            const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)),
+                                                        __dmul_rn(dz, dz));
+                            uw = __double2float_ru(d2 * (1.0 + 9.094947017729282e-13));
+                        }
+                    }
+                    if (tot >= a.prune_min || (COOP && tot >= a.coop_min) || uw < CUDART_INF_F) {
                         face_gaps(sy, g.oy, g.h, cy, gym, gyp);
                         face_gaps(sz, g.oz, g.h, cz, gzm, gzp);
                     }
-                    // (the cooperative instantiation prunes heavy queries only)
-                    if (!COOP && tot >= a.prune_min && fe > fb) {
+                    if (uw < CUDART_INF_F) {
+                        ub = uw;   // no pre-scan needed
+                    } else if (!COOP && tot >= a.prune_min && fe > fb) {
+                        // (the cooperative instantiation prunes heavy queries only)
                         // that row first: the same prefilter scan as pass 1
                         for (int j = fb; j < fe; ++j) {
                             const float4 t = __ldg(&a.tpos[j]);
@@ -453,8 +470,8 @@ __global__ void __launch_bounds__(kK3Threads, 4) k3_balanced(const K3Args a) {
 #pragma unroll
                     for (int t = 0; t < 9; ++t) {
                         const int r = kOrder[t];
-                        if (ee[r] > bb[r] &&
-                            (nseg == 0 || k0 == 0 || !(row_lower(r % 3 - 1, r / 3 - 1, gym, gyp, gzm, gzp) > ub))) {
+                        if (ee[r] > bb[r] && ((k0 == 1 && nseg == 0) || ub == CUDART_INF_F ||
+                                              !(row_lower(r % 3 - 1, r / 3 - 1, gym, gyp, gzm, gzp) > ub))) {
                             segs[nseg * 32 + lane] = make_int2(bb[r], ee[r]);
                             ++nseg;
                             c += ee[r] - bb[r];
@@ -464,6 +481,7 @@ __global__ void __launch_bounds__(kK3Threads, 4) k3_balanced(const K3Args a) {
                     if (COOP) {
                         s_gap[PRUNE ? warp : 0][lane] = make_float4(gym, gyp, gzm, gzp);
                         s_rmask[PRUNE ? warp : 0][lane] = rmask;
+                        s_uw[PRUNE ? warp : 0][lane] = uw;
                     }
                 }
             } else if (g.hashed && near) {
@@ -526,11 +544,12 @@ __global__ void __launch_bounds__(kK3Threads, 4) k3_balanced(const K3Args a) {
             // skipped (§5.2c; warp-uniform decisions)
             const bool cprune = PRUNE && !g.hashed;
             int qmask = 0;
-            float qgym = 0.f, qgyp = 0.f, qgzm = 0.f, qgzp = 0.f, qE1u = 0.f;
+            float qgym = 0.f, qgyp = 0.f, qgzm = 0.f, qgzp = 0.f, qE1u = 0.f, qUw = CUDART_INF_F;
             double qsxw = 0.0;
             if (cprune) {   // (a heavy query is near and dense: its slots were written)
                 qsxw = __shfl_sync(0xffffffffu, sx, q);
                 qmask = s_rmask[PRUNE ? warp : 0][q];
+                qUw = s_uw[PRUNE ? warp : 0][q];
                 const float4 gq = s_gap[PRUNE ? warp : 0][q];
                 qgym = gq.x, qgyp = gq.y, qgzm = gq.z, qgzp = gq.w;
                 qE1u = __double2float_ru(__shfl_sync(0xffffffffu, E1, q));
@@ -553,7 +572,7 @@ __global__ void __launch_bounds__(kK3Threads, 4) k3_balanced(const K3Args a) {
                 qmask &= qmask - 1;
                 const int r = (int)((0x862075314ull >> (4 * t)) & 0xFull);   // kOrder[t]
                 const float Lr = row_lower(r % 3 - 1, r / 3 - 1, qgym, qgyp, qgzm, qgzp);
-                const float ub = prune_ub(lm1, qE1u, r2u);
+                const float ub = fminf(prune_ub(lm1, qE1u, r2u), qUw);
                 if (k > 0 && Lr > ub) continue;
                 int2 sg = segs[k * 32 + q];
                 if (a.xsorted) {
@@ -724,7 +743,7 @@ __global__ void __launch_bounds__(kK3Threads, 4) k3_balanced(const K3Args a) {
             }
         }
         if (WRITE_CORR && i < a.n) a.corr_out[__float_as_int(p.w)] = widx;
-        if (!PRUNE && a.prev_j && i < a.n) a.prev_j[i] = win;   // the next pass's warm start
+        if (a.prev_j && i < a.n) a.prev_j[i] = win;   // the next pass's warm start
 
         // A5: r = (s'-q).n, J = [s' x n ; n] (R4) -> V = (J, r, m), W = (J, m, d2)
         const unsigned matched = __ballot_sync(0xffffffffu, win >= 0);

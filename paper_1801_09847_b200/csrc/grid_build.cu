@@ -110,6 +110,22 @@ __global__ void k_cell_keys(const float* __restrict__ xyz, int64_t n, GridDev g,
     }
 }
 
+// cell starts from the radix-sorted keys: run starts write their position,
+// occupancy bits are set at the same time; a reverse "last defined" scan then
+// gives every empty cell the start of the next occupied one (o3g_api.cu)
+__global__ void k_cs_runs(const uint32_t* __restrict__ keys, int64_t n, int32_t* __restrict__ runs,
+                          int64_t table_size, uint32_t* __restrict__ occ_bits) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t k = keys[i];
+        if (i == 0 || keys[i - 1] != k) {
+            runs[k] = (int32_t)i;
+            if (occ_bits) atomicOr(&occ_bits[k >> 5], 1u << (k & 31));
+        }
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) runs[table_size] = (int32_t)n;
+}
+
 // hashed grid: occupancy of coarse cells (2^shift fine cells per axis), the
 // live-query test's structure when no dense per-cell bitmap fits
 __global__ void k_coarse_bits(const float4* __restrict__ tpos, int64_t n, GridDev g, int shift, int cnx, int cny,
@@ -281,6 +297,10 @@ void launch_cell_keys(const float* xyz, int64_t n, const GridDev& g, const doubl
     k_cell_keys<<<blocks_for(n, 256), 256, 0, s>>>(xyz, n, g, T != nullptr, t[0], t[1], t[2], t[3],
                                                    t[4], t[5], t[6], t[7], t[8], t[9], t[10], t[11],
                                                    keys, vals, brick);
+}
+void launch_cs_runs(const uint32_t* keys, int64_t n, int32_t* runs, int64_t table_size, uint32_t* occ_bits,
+                    cudaStream_t s) {
+    k_cs_runs<<<blocks_for(n, 256), 256, 0, s>>>(keys, n, runs, table_size, occ_bits);
 }
 void launch_coarse_bits(const float4* tpos, int64_t n, const GridDev& g, int shift, int cnx, int cny,
                         uint32_t* bits, cudaStream_t s) {

@@ -10,6 +10,7 @@
 #include <cub/device/device_select.cuh>
 #include <cub/iterator/counting_input_iterator.cuh>
 #include <algorithm>
+#include <thrust/iterator/reverse_iterator.h>
 #include <string>
 #include <vector>
 
@@ -102,6 +103,12 @@ NcclApi& nccl() {
     return api;
 }
 }  // namespace
+
+// "last defined" (>= 0) value: a reverse inclusive scan with it fills every
+// empty cell's start with the next occupied cell's start
+struct LastDefined {
+    __host__ __device__ int32_t operator()(int32_t acc, int32_t v) const { return v >= 0 ? v : acc; }
+};
 
 // ------------------------------------------------------------------ ctx
 struct GraphKey {
@@ -447,15 +454,39 @@ static o3g_status set_target_impl(o3g_ctx* c, const float* xyz, const float* nor
 
     launch_cell_keys(dx, n, g, nullptr, c->keys_a.as<uint32_t>(), c->vals_a.as<int32_t>(), c->exec);
     const bool radix = c->target_sort == 1;
-    if (radix) TRY(sort_pairs(c, n, bits_for((uint64_t)(g.table_size - 1))));
-    CK(cudaMemsetAsync(c->counts.p, 0, (g.table_size + 1) * 4, c->exec));
-    launch_histogram(c->keys_a.as<uint32_t>(), n, c->counts.as<int32_t>(), radix ? nullptr : occ, c->exec);
-    size_t tmp = 0;
-    CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, c->counts.as<int32_t>(), c->cell_start.as<int32_t>(),
-                                     (int)(g.table_size + 1), c->exec));
-    TRY(c->cub_tmp.ensure(tmp));
-    CK(cub::DeviceScan::ExclusiveSum(c->cub_tmp.p, tmp, c->counts.as<int32_t>(), c->cell_start.as<int32_t>(),
-                                     (int)(g.table_size + 1), c->exec));
+    bool occ_built = false;
+    if (radix) {
+        TRY(sort_pairs(c, n, bits_for((uint64_t)(g.table_size - 1))));
+        // cell starts from the sorted keys (no histogram): run starts, then a
+        // reverse last-defined scan; dense grids get their occupancy bits here
+        uint32_t* obits = nullptr;
+        if (!g.hashed) {
+            const int64_t nw = (g.table_size + 31) / 32;
+            TRY(c->nbr_a.ensure(nw * 4));
+            TRY(c->nbr_b.ensure(nw * 4));
+            CK(cudaMemsetAsync(c->nbr_a.p, 0, nw * 4, c->exec));
+            obits = c->nbr_a.as<uint32_t>();
+            occ_built = true;
+        }
+        CK(cudaMemsetAsync(c->counts.p, 0xFF, (g.table_size + 1) * 4, c->exec));
+        launch_cs_runs(c->keys_b.as<uint32_t>(), n, c->counts.as<int32_t>(), g.table_size, obits, c->exec);
+        thrust::reverse_iterator<int32_t*> rin(c->counts.as<int32_t>() + g.table_size + 1);
+        thrust::reverse_iterator<int32_t*> rout(c->cell_start.as<int32_t>() + g.table_size + 1);
+        size_t tmp = 0;
+        CK(cub::DeviceScan::InclusiveScan(nullptr, tmp, rin, rout, LastDefined(), (int)(g.table_size + 1), c->exec));
+        TRY(c->cub_tmp.ensure(tmp));
+        CK(cub::DeviceScan::InclusiveScan(c->cub_tmp.p, tmp, rin, rout, LastDefined(), (int)(g.table_size + 1),
+                                          c->exec));
+    } else {
+        CK(cudaMemsetAsync(c->counts.p, 0, (g.table_size + 1) * 4, c->exec));
+        launch_histogram(c->keys_a.as<uint32_t>(), n, c->counts.as<int32_t>(), occ, c->exec);
+        size_t tmp = 0;
+        CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, c->counts.as<int32_t>(), c->cell_start.as<int32_t>(),
+                                         (int)(g.table_size + 1), c->exec));
+        TRY(c->cub_tmp.ensure(tmp));
+        CK(cub::DeviceScan::ExclusiveSum(c->cub_tmp.p, tmp, c->counts.as<int32_t>(), c->cell_start.as<int32_t>(),
+                                         (int)(g.table_size + 1), c->exec));
+    }
     if (normals_ready) {
         CK(cudaStreamWaitEvent(c->exec, normals_ready, 0));
         if (dn) {
@@ -478,8 +509,13 @@ static o3g_status set_target_impl(o3g_ctx* c, const float* xyz, const float* nor
         const int64_t nw = (g.table_size + 31) / 32;
         TRY(c->nbr_a.ensure(nw * 4));
         TRY(c->nbr_b.ensure(nw * 4));
-        launch_nbr_bits(c->cell_start.as<int32_t>(), g.table_size, g.nx, (int64_t)g.nx * g.ny,
-                        c->nbr_b.as<uint32_t>(), c->nbr_a.as<uint32_t>(), c->exec);
+        if (occ_built) {   // occupancy bits already set from the sorted keys: dilate only
+            launch_dilate3(c->nbr_a.as<uint32_t>(), c->nbr_b.as<uint32_t>(), g.table_size, g.nx,
+                           (int64_t)g.nx * g.ny, c->exec);
+        } else {
+            launch_nbr_bits(c->cell_start.as<int32_t>(), g.table_size, g.nx, (int64_t)g.nx * g.ny,
+                            c->nbr_b.as<uint32_t>(), c->nbr_a.as<uint32_t>(), c->exec);
+        }
         c->launches += 4;
         c->nbr_ready = true;
     } else {

@@ -110,20 +110,18 @@ __global__ void k_cell_keys(const float* __restrict__ xyz, int64_t n, GridDev g,
     }
 }
 
-// cell starts from the radix-sorted keys: run starts write their position,
-// occupancy bits are set at the same time; a reverse "last defined" scan then
-// gives every empty cell the start of the next occupied one (o3g_api.cu)
+// cell starts from the radix-sorted keys: each occupied cell k records the end
+// of its run (runs[k], zero elsewhere) and its occupancy bit; an exclusive max
+// scan then gives cell c the end of the last occupied cell before c, i.e. the
+// number of points with key < c (o3g_api.cu)
 __global__ void k_cs_runs(const uint32_t* __restrict__ keys, int64_t n, int32_t* __restrict__ runs,
-                          int64_t table_size, uint32_t* __restrict__ occ_bits) {
+                          uint32_t* __restrict__ occ_bits) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
         const uint32_t k = keys[i];
-        if (i == 0 || keys[i - 1] != k) {
-            runs[k] = (int32_t)i;
-            if (occ_bits) atomicOr(&occ_bits[k >> 5], 1u << (k & 31));
-        }
+        if (i == n - 1 || keys[i + 1] != k) runs[k] = (int32_t)(i + 1);
+        if (occ_bits && (i == 0 || keys[i - 1] != k)) atomicOr(&occ_bits[k >> 5], 1u << (k & 31));
     }
-    if (blockIdx.x == 0 && threadIdx.x == 0) runs[table_size] = (int32_t)n;
 }
 
 // hashed grid: occupancy of coarse cells (2^shift fine cells per axis), the
@@ -298,9 +296,8 @@ void launch_cell_keys(const float* xyz, int64_t n, const GridDev& g, const doubl
                                                    t[4], t[5], t[6], t[7], t[8], t[9], t[10], t[11],
                                                    keys, vals, brick);
 }
-void launch_cs_runs(const uint32_t* keys, int64_t n, int32_t* runs, int64_t table_size, uint32_t* occ_bits,
-                    cudaStream_t s) {
-    k_cs_runs<<<blocks_for(n, 256), 256, 0, s>>>(keys, n, runs, table_size, occ_bits);
+void launch_cs_runs(const uint32_t* keys, int64_t n, int32_t* runs, uint32_t* occ_bits, cudaStream_t s) {
+    k_cs_runs<<<blocks_for(n, 256), 256, 0, s>>>(keys, n, runs, occ_bits);
 }
 void launch_coarse_bits(const float4* tpos, int64_t n, const GridDev& g, int shift, int cnx, int cny,
                         uint32_t* bits, cudaStream_t s) {

@@ -10,7 +10,6 @@
 #include <cub/device/device_select.cuh>
 #include <cub/iterator/counting_input_iterator.cuh>
 #include <algorithm>
-#include <thrust/iterator/reverse_iterator.h>
 #include <string>
 #include <vector>
 
@@ -103,12 +102,6 @@ NcclApi& nccl() {
     return api;
 }
 }  // namespace
-
-// "last defined" (>= 0) value: a reverse inclusive scan with it fills every
-// empty cell's start with the next occupied cell's start
-struct LastDefined {
-    __host__ __device__ int32_t operator()(int32_t acc, int32_t v) const { return v >= 0 ? v : acc; }
-};
 
 // ------------------------------------------------------------------ ctx
 struct GraphKey {
@@ -457,8 +450,8 @@ static o3g_status set_target_impl(o3g_ctx* c, const float* xyz, const float* nor
     bool occ_built = false;
     if (radix) {
         TRY(sort_pairs(c, n, bits_for((uint64_t)(g.table_size - 1))));
-        // cell starts from the sorted keys (no histogram): run starts, then a
-        // reverse last-defined scan; dense grids get their occupancy bits here
+        // cell starts from the sorted keys (no histogram): run ends, then an
+        // exclusive max scan; dense grids get their occupancy bits here
         uint32_t* obits = nullptr;
         if (!g.hashed) {
             const int64_t nw = (g.table_size + 31) / 32;
@@ -468,15 +461,14 @@ static o3g_status set_target_impl(o3g_ctx* c, const float* xyz, const float* nor
             obits = c->nbr_a.as<uint32_t>();
             occ_built = true;
         }
-        CK(cudaMemsetAsync(c->counts.p, 0xFF, (g.table_size + 1) * 4, c->exec));
-        launch_cs_runs(c->keys_b.as<uint32_t>(), n, c->counts.as<int32_t>(), g.table_size, obits, c->exec);
-        thrust::reverse_iterator<int32_t*> rin(c->counts.as<int32_t>() + g.table_size + 1);
-        thrust::reverse_iterator<int32_t*> rout(c->cell_start.as<int32_t>() + g.table_size + 1);
+        CK(cudaMemsetAsync(c->counts.p, 0, (g.table_size + 1) * 4, c->exec));
+        launch_cs_runs(c->keys_b.as<uint32_t>(), n, c->counts.as<int32_t>(), obits, c->exec);
         size_t tmp = 0;
-        CK(cub::DeviceScan::InclusiveScan(nullptr, tmp, rin, rout, LastDefined(), (int)(g.table_size + 1), c->exec));
+        CK(cub::DeviceScan::ExclusiveScan(nullptr, tmp, c->counts.as<int32_t>(), c->cell_start.as<int32_t>(),
+                                          cub::Max(), (int32_t)0, (int)(g.table_size + 1), c->exec));
         TRY(c->cub_tmp.ensure(tmp));
-        CK(cub::DeviceScan::InclusiveScan(c->cub_tmp.p, tmp, rin, rout, LastDefined(), (int)(g.table_size + 1),
-                                          c->exec));
+        CK(cub::DeviceScan::ExclusiveScan(c->cub_tmp.p, tmp, c->counts.as<int32_t>(), c->cell_start.as<int32_t>(),
+                                          cub::Max(), (int32_t)0, (int)(g.table_size + 1), c->exec));
     } else {
         CK(cudaMemsetAsync(c->counts.p, 0, (g.table_size + 1) * 4, c->exec));
         launch_histogram(c->keys_a.as<uint32_t>(), n, c->counts.as<int32_t>(), occ, c->exec);

@@ -88,8 +88,7 @@ void launch_check_finite(const float* v, int64_t count, int32_t* nonfinite, int 
 // needs < 2^10 bricks per axis), 0: the table index
 void launch_cell_keys(const float* xyz, int64_t n, const GridDev& g, const double* T12_or_null,
                       uint32_t* keys, int32_t* vals, cudaStream_t s, int brick = 0);
-void launch_cs_runs(const uint32_t* keys, int64_t n, int32_t* runs, int64_t table_size, uint32_t* occ_bits,
-                    cudaStream_t s);
+void launch_cs_runs(const uint32_t* keys, int64_t n, int32_t* runs, uint32_t* occ_bits, cudaStream_t s);
 void launch_dilate3(uint32_t* bits, uint32_t* tmp, int64_t ncells, int64_t nx, int64_t nxny, cudaStream_t s);
 void launch_coarse_bits(const float4* tpos, int64_t n, const GridDev& g, int shift, int cnx, int cny,
                         uint32_t* bits, cudaStream_t s);

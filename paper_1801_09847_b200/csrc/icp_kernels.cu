@@ -347,6 +347,7 @@ __global__ void __launch_bounds__(kK3Threads, 4) k3_balanced(const K3Args a) {
         float4 p = make_float4(0.f, 0.f, 0.f, 0.f);
         if (i < a.n) {
             p = __ldg(&a.src[i]);
+            const int jprev = warm ? __ldg(&a.prev_j[i]) : -1;   // previous pass's winner (warm start)
             xform_rn(sT, p.x, p.y, p.z, sx, sy, sz);
             const int cx = cell_coord(sx, g.ox, g.inv_h, g.nx);
             const int cy = cell_coord(sy, g.oy, g.inv_h, g.ny);
@@ -387,7 +388,7 @@ __global__ void __launch_bounds__(kK3Threads, 4) k3_balanced(const K3Args a) {
                     float ub = CUDART_INF_F;
                     float gym = 0.f, gyp = 0.f, gzm = 0.f, gzp = 0.f;
                     if (warm) {
-                        const int jp = __ldg(&a.prev_j[i]);
+                        const int jp = jprev;
                         if (jp >= 0) {
                             const float4 t = __ldg(&a.tpos[jp]);
                             const double dx = __dsub_rn(sx, (double)t.x), dy = __dsub_rn(sy, (double)t.y),
@@ -430,7 +431,7 @@ __global__ void __launch_bounds__(kK3Threads, 4) k3_balanced(const K3Args a) {
                     // fp64 d2 bounds this pass's winner (see the plain path)
                     float uw = CUDART_INF_F;
                     if (warm) {
-                        const int jp = __ldg(&a.prev_j[i]);
+                        const int jp = jprev;
                         if (jp >= 0) {
                             const float4 t = __ldg(&a.tpos[jp]);
                             const double dx = __dsub_rn(sx, (double)t.x), dy = __dsub_rn(sy, (double)t.y),
@@ -485,8 +486,21 @@ __global__ void __launch_bounds__(kK3Threads, 4) k3_balanced(const K3Args a) {
                     }
                 }
             } else if (g.hashed && near) {
+                // warm start (as on the dense grid): rows beyond the previous
+                // winner's bound are not looked up
+                float ub = CUDART_INF_F, hym = 0.f, hyp = 0.f, hzm = 0.f, hzp = 0.f;
+                if (jprev >= 0) {
+                    const float4 t = __ldg(&a.tpos[jprev]);
+                    const double dx = __dsub_rn(sx, (double)t.x), dy = __dsub_rn(sy, (double)t.y),
+                                 dz = __dsub_rn(sz, (double)t.z);
+                    const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+                    ub = __double2float_ru(d2 * (1.0 + 9.094947017729282e-13));
+                    face_gaps(sy, g.oy, g.h, cy, hym, hyp);
+                    face_gaps(sz, g.oz, g.h, cz, hzm, hzp);
+                }
                 for (int z = zlo; z <= zhi; ++z) {
                     for (int y = ylo; y <= yhi; ++y) {
+                        if (ub < CUDART_INF_F && row_lower(y - cy, z - cz, hym, hyp, hzm, hzp) > ub) continue;
                         int b0, e0, b1 = 0, e1 = 0;
                         if (!g.hashed) {
                             const int rb = (z * g.ny + y) * g.nx;   // < table_size < 2^31

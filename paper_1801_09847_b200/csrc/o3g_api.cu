@@ -593,10 +593,8 @@ o3g_status o3g_set_source(o3g_ctx* c, const float* xyz, int64_t n, const double 
     int32_t* bad = (int32_t*)(c->misc.as<uint32_t>() + 6);
     CK(cudaMemsetAsync(bad, 0, 4, c->exec));
     launch_check_finite(dx, 3 * n, bad, c->sms, c->exec);
-    int32_t h_bad = 0;
-    CK(cudaMemcpyAsync(&h_bad, bad, 4, cudaMemcpyDeviceToHost, c->exec));
-    CK(cudaStreamSynchronize(c->exec));
-    if (h_bad) return fail(O3G_ERR_INVALID_ARGUMENT, "non-finite source coordinate");
+    // (the flag is read at the final sync: a non-finite point only yields a
+    // clamped ordering key meanwhile, and the call then fails)
 
     TRY(c->keys_a.ensure(n * 4));
     TRY(c->keys_b.ensure(n * 4));
@@ -646,8 +644,11 @@ o3g_status o3g_set_source(o3g_ctx* c, const float* xyz, int64_t n, const double 
         CK(cudaMemcpyAsync(&c->ntiles, nsel, 4, cudaMemcpyDeviceToHost, c->exec));
         c->launches += 5;
     }
+    int32_t h_bad = 0;
+    CK(cudaMemcpyAsync(&h_bad, (int32_t*)(c->misc.as<uint32_t>() + 6), 4, cudaMemcpyDeviceToHost, c->exec));
     CK(cudaStreamSynchronize(c->exec));
     CK(cudaGetLastError());
+    if (h_bad) return fail(O3G_ERR_INVALID_ARGUMENT, "non-finite source coordinate");
     c->n_total = n;
     c->n_local = hi - lo;
     c->shard_lo = lo;

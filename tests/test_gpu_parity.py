@@ -291,6 +291,15 @@ def test_invalid_arguments(o3g, workloads):
         o3g.icp_point_to_plane(w["source"], w["target"], w["target_normals"], 0.05, relative_rmse=-1)
     with pytest.raises(E):
         o3g.icp_point_to_plane(w["source"], w["target"], None, 0.05)
+    # option ranges (include/o3g.h): every invalid value is rejected, valid ones accepted
+    with o3g.Context(0) as ctx:
+        for opt, bad_v in ((1, 5), (1, -1), (2, 3), (4, 65), (6, -2), (7, 2), (8, 2), (9, 2), (10, -4),
+                           (11, 2), (11, -2), (12, 2), (99, 0)):
+            with pytest.raises(E):
+                ctx.set_option(opt, bad_v)
+        for opt, ok_v in ((1, 4), (2, 0), (3, 1), (4, 0), (5, 0), (6, -1), (7, 0), (8, 1), (9, 0), (10, -2),
+                          (11, -1), (12, -1)):
+            ctx.set_option(opt, ok_v)
 
 
 def test_flags_no_corr_and_degenerate(o3g, workloads):

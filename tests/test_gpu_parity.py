@@ -510,3 +510,24 @@ def test_loop_parity_warm_start(o3g, workloads):
         assert r.iterations == ref["iterations"]
         n = min(len(r.hist_fitness), len(ref["hist_fitness"]))
         assert np.abs(r.hist_fitness[:n] - ref["hist_fitness"][:n]).max() <= 1e-6
+
+
+@pytest.mark.slow
+def test_large16m_converged_regime_sampled(o3g, workloads):
+    """BASELINE config 5 at full size started near T* (every query live: the
+    live-query queue is skipped after the first pass and every pass after the
+    first runs warm-started): the loop's result satisfies S:305 and a step at
+    the returned T matches the oracle on sampled queries."""
+    w = workloads("large16m")
+    T0 = w["T_true"] @ _perturb(41, 0.0017, 0.01)
+    sub = Stream(42).integers(20000, len(w["source"]))
+    grid = oracle.Grid(w["target"], w["dmax"])
+    with _ctx(o3g, w, order_T=T0) as ctx:
+        r = ctx.run(T0, 5, 0.0, 0.0, history=True)
+        corr, st = _step(ctx, r.transformation, len(w["source"]))
+    assert r.fitness > 0.9 and r.iterations == 5
+    assert st["count"] / len(w["source"]) == r.fitness
+    assert abs(np.sqrt(st["sum_sq_dist"] / st["count"]) - r.inlier_rmse) <= 1e-12 * r.inlier_rmse
+    ref = oracle.step(r.transformation, w["source"], w["target"], w["target_normals"], w["dmax"],
+                      grid=grid, subset=sub)
+    assert np.array_equal(corr[sub], ref["corr"])

@@ -251,8 +251,11 @@ o3g_status o3g_dist_init(o3g_ctx* ctx, int rank, int world, const void* nccl_uni
  * O3G_OPT_PRUNE_MIN: variant 1, dense grid: a query with at least this
  *   many candidates first scans one x-row, then skips the rows whose lower
  *   distance bound exceeds that row's best; -1 = auto
- *   (default: threshold 32 when the target averages >= 4 points per
- *   occupied cell, else off), -2 = never, 0 = every query.
+ *   (default: threshold 32 when the target averages 4 to 32 points per
+ *   occupied cell; above 32 only the cooperative path prunes; below 4 off),
+ *   -2 = never, 0 = every query. Independently, o3g_icp_run's passes after
+ *   the first bound every query by its previous winner (warm start).
+ *   Results are identical either way.
  * O3G_OPT_INTERLEAVE: variant 1 batch composition: 0 = 32 consecutive
  *   queries of the ordered source per warp batch; 1 = lane l of batch b
  *   takes query l * ceil(n/32) + b (spreads clustered heavy queries over

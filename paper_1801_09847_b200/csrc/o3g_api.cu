@@ -664,16 +664,17 @@ static int coop_min_of(const o3g_ctx* c) {
 }
 
 // row pruning (variant 1, dense grid): the per-query candidate threshold, or
-// -1 for the plain instantiation. auto: on when the target averages 4 to 32
-// points per occupied cell (measured: depth -21% K3, fragment -8% step; the
-// sparse large16m, 1.7 per cell, loses 5% to the pre-scan; LiDAR, 226 per
-// cell and cooperative, loses 4%), threshold 32
+// -1 for the plain instantiation (before the warm start, the pre-scan form
+// gained 21% K3 on depth and 8% on fragment; with it, it costs ~2%)
 static int prune_of(const o3g_ctx* c) {
     if (c->g.hashed || c->prune_min == -2) return -1;
     if (c->prune_min >= 0) return c->prune_min;
     const double rho = (double)c->m / (double)(c->occupied > 0 ? c->occupied : 1);
-    // >= 32 per cell: the cooperative path prunes its rows; no light pre-scan
-    return rho >= 32.0 ? (1 << 30) : rho >= 4.0 ? 32 : -1;
+    // >= 32 per cell: the cooperative path prunes its rows (no light pre-scan).
+    // Below that the run loop's warm start already prunes every pass after
+    // the first, and the pre-scan instantiation measured slower (depth 1.774
+    // vs 1.811 ms, fragment 10.87 vs 11.04 ms per step): off.
+    return rho >= 32.0 ? (1 << 30) : -1;
 }
 
 // point-to-point runs on the two-pass kernel

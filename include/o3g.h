@@ -232,7 +232,7 @@ o3g_status o3g_dist_init(o3g_ctx* ctx, int rank, int world, const void* nccl_uni
  *   dilated occupancy bitmap of the dense grid (default), 0 = off.
  * O3G_OPT_COOP_MIN: variant 1 scans a query with at least this many
  *   candidates with the whole warp (0 = never; -1 = auto, the default:
- *   256 when the target averages >= 32 points per occupied cell, else 0).
+ *   32 when the target averages >= 32 points per occupied cell, else 0).
  * O3G_OPT_ESTIMATION: 0 = point-to-plane (default), 1 = point-to-point
  *   (TransformationEstimationPointToPoint(False); SPEC
  *   S:255-263): Horn's closed-form rigid fit on the correspondences, no

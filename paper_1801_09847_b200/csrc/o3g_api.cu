@@ -658,9 +658,11 @@ o3g_status o3g_set_source(o3g_ctx* c, const float* xyz, int64_t n, const double 
 
 static int coop_min_of(const o3g_ctx* c) {
     // auto (-1): warp-cooperative scans only where cells are dense (measured:
-    // LiDAR, 226 points per occupied cell, gains 2.3x; sparse configs lose)
+    // LiDAR, 226 points per occupied cell, gains 2.3x; sparse configs lose);
+    // threshold 32 (with the warm start and x-windows, LiDAR K3 0.240 ms for
+    // thresholds 1-32 vs 0.250 at 256)
     return c->coop_min >= 0 ? c->coop_min
-                            : ((double)c->m >= 32.0 * (double)(c->occupied > 0 ? c->occupied : 1) ? 256 : 0);
+                            : ((double)c->m >= 32.0 * (double)(c->occupied > 0 ? c->occupied : 1) ? 32 : 0);
 }
 
 // row pruning (variant 1, dense grid): the per-query candidate threshold, or

@@ -440,8 +440,12 @@ __global__ void __launch_bounds__(kK3Threads, 4) k3_balanced(const K3Args a) {
                         face_gaps(sy, g.oy, g.h, cy, gym, gyp);
                         face_gaps(sz, g.oz, g.h, cz, gzm, gzp);
                     }
+                    float gxm2 = 0.f, gxp2 = 0.f;   // (warm) x-gaps of the end cells, squared
                     if (uw < CUDART_INF_F) {
                         ub = uw;   // no pre-scan needed
+                        float gxm, gxp;
+                        face_gaps(sx, g.ox, g.h, cx, gxm, gxp);
+                        gxm2 = __fmul_rd(gxm, gxm), gxp2 = __fmul_rd(gxp, gxp);
                     } else if (!COOP && tot >= a.prune_min && fe > fb) {
                         // (the cooperative instantiation prunes heavy queries only)
                         // that row first: the same prefilter scan as pass 1
@@ -468,10 +472,20 @@ __global__ void __launch_bounds__(kK3Threads, 4) k3_balanced(const K3Args a) {
                         const int r = kOrder[t];
                         if (ee[r] > bb[r] && ((k0 == 1 && nseg == 0) || ub == CUDART_INF_F ||
                                               !(row_lower(r % 3 - 1, r / 3 - 1, gym, gyp, gzm, gzp) > ub))) {
-                            segs[nseg * 32 + lane] = make_int2(bb[r], ee[r]);
-                            ++nseg;
-                            c += ee[r] - bb[r];
-                            rmask |= 1 << t;
+                            int b = bb[r], e = ee[r];
+                            if (uw < CUDART_INF_F && w == 3) {
+                                // warm: an end cell (cx -+ 1) with L_row + gx^2 > ub is cut
+                                const float Lr = row_lower(r % 3 - 1, r / 3 - 1, gym, gyp, gzm, gzp);
+                                const int rb = rb0 + (r / 3) * nxny + (r % 3) * g.nx;
+                                if (__fadd_rd(Lr, gxm2) > ub) b = __ldg(cs + rb + 1);
+                                if (__fadd_rd(Lr, gxp2) > ub) e = __ldg(cs + rb + 2);
+                            }
+                            if (e > b) {
+                                segs[nseg * 32 + lane] = make_int2(b, e);
+                                ++nseg;
+                                c += e - b;
+                                rmask |= 1 << t;
+                            }
                         }
                     }
                     if (COOP) {

@@ -676,7 +676,7 @@ static int prune_of(const o3g_ctx* c) {
     // Below that the run loop's warm start already prunes every pass after
     // the first, and the pre-scan instantiation measured slower (depth 1.774
     // vs 1.811 ms, fragment 10.87 vs 11.04 ms per step): off.
-    return rho >= 32.0 ? (1 << 30) : -1;
+    return rho >= 4.0 ? (1 << 30) : -1;
 }
 
 // point-to-point runs on the two-pass kernel

@@ -251,9 +251,10 @@ o3g_status o3g_dist_init(o3g_ctx* ctx, int rank, int world, const void* nccl_uni
  * O3G_OPT_PRUNE_MIN: variant 1, dense grid: a query with at least this
  *   many candidates first scans one x-row, then skips the rows whose lower
  *   distance bound exceeds that row's best; -1 = auto
- *   (default: only the cooperative path prunes, for targets averaging >= 32
- *   points per occupied cell; the light-query pre-scan is off by default
- *   since the run loop's warm start prunes every pass after the first),
+ *   (default: for targets averaging >= 4 points per occupied cell, the
+ *   pruning kernel without the light-query pre-scan — the run loop's warm
+ *   start prunes every pass after the first and cuts end cells of rows —
+ *   and, at >= 32, the cooperative path's row pruning; else off),
  *   -2 = never, 0 = every query. Independently, o3g_icp_run's passes after
  *   the first bound every query by its previous winner (warm start).
  *   Results are identical either way.

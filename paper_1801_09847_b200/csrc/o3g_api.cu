@@ -672,10 +672,10 @@ static int prune_of(const o3g_ctx* c) {
     if (c->g.hashed || c->prune_min == -2) return -1;
     if (c->prune_min >= 0) return c->prune_min;
     const double rho = (double)c->m / (double)(c->occupied > 0 ? c->occupied : 1);
-    // >= 32 per cell: the cooperative path prunes its rows (no light pre-scan).
-    // Below that the run loop's warm start already prunes every pass after
-    // the first, and the pre-scan instantiation measured slower (depth 1.774
-    // vs 1.811 ms, fragment 10.87 vs 11.04 ms per step): off.
+    // >= 4 per cell: the pruning instantiation without the light pre-scan
+    // (the warm start supersedes it), for its warm-start cell cuts and, at
+    // >= 32 per cell, the cooperative path's row pruning (depth K3 0.044 ->
+    // 0.041 ms, LiDAR 0.240 -> 0.189; the sparse large16m loses: off there)
     return rho >= 4.0 ? (1 << 30) : -1;
 }
 

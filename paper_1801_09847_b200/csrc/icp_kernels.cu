@@ -274,11 +274,11 @@ __global__ void __launch_bounds__(kK3Threads, 4) k3_balanced(const K3Args a) {
     // full search runs on full warps of live queries only.
     __shared__ int qbuf[kK3Threads / 32][64];
     // the live-query pre-pass pays while many queries have nothing in reach;
-    // once the previous pass matched most of the source (fitness > 0.7,
-    // e.g. near convergence) it is skipped (measured on large16m: queue 0.650
-    // vs 0.733 ms at T_init, 1.145 vs 1.039 ms converged). Results are the
-    // same either way.
-    const bool use_queue = a.nbr_bits != nullptr && !(!a.eval_T && a.st->passes > 0 && a.st->fit > 0.7);
+    // once the previous pass matched at least half of the source it is
+    // skipped (measured: large16m queue 0.650 vs 0.733 ms at T_init (fitness
+    // 0.36), 1.145 vs 1.039 ms converged; fragment (fitness 0.55) step 11.01
+    // -> 10.64 ms with 0.5 instead of 0.7). Results are the same either way.
+    const bool use_queue = a.nbr_bits != nullptr && !(!a.eval_T && a.st->passes > 0 && a.st->fit > 0.5);
     const bool warm = a.prev_j && !a.eval_T && a.st->passes > 0;
     __shared__ float4 s_gap[PRUNE && COOP ? kK3Threads / 32 : 1][32];
     __shared__ int s_rmask[PRUNE && COOP ? kK3Threads / 32 : 1][32];

@@ -221,8 +221,10 @@ o3g_status o3g_dist_init(o3g_ctx* ctx, int rank, int world, const void* nccl_uni
  *   warp kernel (fp32 prefilter with a proven margin + exact fp64 decision;
  *   the default); 2 = single-pass fp32 prefilter + exact decision; 3 =
  *   two-pass kernel on count-sorted 128-query tiles; 4 = two-pass kernel on
- *   512-query tiles whose target neighbourhood is staged in shared memory
- *   (dense grid; a hashed grid runs variant 1).
+ *   tiles of <= 128 queries (source in 8^3-brick Morton order, set at the next
+ *   o3g_set_source) whose target neighbourhood is staged in shared memory
+ *   (dense grid; a hashed grid runs variant 1). Point-to-point estimation and
+ *   batched evaluation always run variant 1.
  * O3G_OPT_GRID: 0 = auto, 1 = force dense cell table, 2 = force hashed
  *   cell table (collisions only add candidates; results are identical).
  * O3G_OPT_TIMING: 1 = record CUDA events around every correspondence

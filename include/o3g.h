@@ -268,11 +268,25 @@ o3g_status o3g_dist_init(o3g_ctx* ctx, int rank, int world, const void* nccl_uni
  *   o3g_set_target) so the cooperative path scans, per x-row, only the
  *   window |q_x - s'_x| <= sqrt(ub - L) found by a warp-wide search
  *   (DESIGN.md §5.2c); -1 = auto (default: >= 32 points per occupied cell).
+ * O3G_OPT_CERT: correspondence certificates in o3g_icp_run (variant 1;
+ *   DESIGN.md §5.5): each full search leaves a per-query radius rho such
+ *   that its answer provably holds while the transformed query moves by
+ *   less than rho (half the gap between the nearest and second-nearest
+ *   target, or the clearance beyond dmax when there is no winner); later
+ *   passes check the displacement |(T_k - T_b) s| against rho and search
+ *   only the queries whose certificate expired. A pass runs this way once the
+ *   previous pass matched more than half of the source (the refinement
+ *   phase); earlier passes run the plain search. -1 = auto (default: shards
+ *   of >= 2^20 queries), 1 = on, 0 = off (the previous winner then only
+ *   bounds the next search, the warm start).
+ * O3G_OPT_TRACE_PASS: k >= 0 = o3g_icp_run also writes the correspondences
+ *   of pass k (original source order) for o3g_last_run_trace; -1 = off
+ *   (default). A testing hook: it adds a scattered index write to pass k.
  * Results are identical for every value of the other options.           */
 enum { O3G_OPT_SEARCH = 1, O3G_OPT_GRID = 2, O3G_OPT_TIMING = 3, O3G_OPT_BLOCKS_PER_SM = 4,
        O3G_OPT_NBR_MASK = 5, O3G_OPT_COOP_MIN = 6, O3G_OPT_ESTIMATION = 7,
        O3G_OPT_SOURCE_ORDER = 8, O3G_OPT_TARGET_SORT = 9, O3G_OPT_PRUNE_MIN = 10,
-       O3G_OPT_INTERLEAVE = 11, O3G_OPT_XSORT = 12 };
+       O3G_OPT_INTERLEAVE = 11, O3G_OPT_XSORT = 12, O3G_OPT_CERT = 13, O3G_OPT_TRACE_PASS = 14 };
 o3g_status o3g_set_option(o3g_ctx* ctx, int option, int64_t value);
 
 /* Sum of the correspondence-kernel (K3) durations of the last o3g_icp_run
@@ -280,6 +294,22 @@ o3g_status o3g_set_option(o3g_ctx* ctx, int option, int64_t value);
  * tail-kernel total. Milliseconds.                                      */
 o3g_status o3g_last_run_kernel_ms(o3g_ctx* ctx, double* k3_ms, int32_t* k3_launches,
                                   double* tail_ms);
+
+/* Per-pass record of the last o3g_icp_run (verification hook, the run-loop
+ * analogue of o3g_icp_step): T_hist [passes][16] the T each pass ran with,
+ * terms_hist [passes][O3G_NTERMS] that pass's 29 terms (same layout as
+ * o3g_icp_step's terms_out), and corr_out [n_source] the correspondences of
+ * pass O3G_OPT_TRACE_PASS in original source order (-1 = none; host or
+ * device memory; untouched if that pass did not run), and stats_hist
+ * [passes][3] per pass: the queries that ran the full correspondence search,
+ * the candidates those searches scanned, and the queries settled by a valid
+ * certificate (the rest had an empty 27-cell stencil) (variant 1; 0 for the
+ * other variants).
+ * passes = info.passes of that run; on a multi-GPU context corr_out holds
+ * this rank's shard only (other entries -2) and stats_hist this rank's
+ * counts. Any pointer may be NULL.                                         */
+o3g_status o3g_last_run_trace(o3g_ctx* ctx, double* T_hist, double* terms_hist, int32_t* corr_out,
+                              double* stats_hist);
 
 /* Grid statistics of the current target: cells per axis, table entries,
  * hashed (0/1), occupied cells. Any pointer may be NULL.                 */

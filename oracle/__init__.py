@@ -18,7 +18,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "o3g_oracle.c")
 _LIB = os.path.join(_HERE, "liborc.so")
-CFLAGS = ["-O2", "-ffp-contract=off", "-fno-fast-math", "-std=c99", "-fPIC", "-shared"]
+CFLAGS = ["-O2", "-ffp-contract=off", "-fno-fast-math", "-std=c99", "-fPIC", "-shared", "-fopenmp"]
 
 NTERMS = 29
 FLAG_NO_CORR = 1
@@ -50,13 +50,15 @@ def lib():
         L.orc_nn_grid.restype = I64
         L.orc_nn_grid.argtypes = [P, P, D, P]
         L.orc_pass_subset.argtypes = [P, P, I64, P, I64, P, P, I64, P, D, P, P, P, P]
+        L.orc_pass_chunked.restype = C.c_int
+        L.orc_pass_chunked.argtypes = [P, P, I64, P, I64, P, P, I64, P, D, P, P, P, P, I32]
         L.orc_expand_jtj.argtypes = [P, P]
         L.orc_ldlt_solve.restype = C.c_int
         L.orc_ldlt_solve.argtypes = [P, P, P]
         L.orc_exp_se3.argtypes = [P, P]
         L.orc_compose.argtypes = [P, P, P]
         L.orc_icp.restype = C.c_int
-        L.orc_icp.argtypes = [P, I64, P, P, I64, P, D, I32, D, D, I32, P, P, P, P, P, P, P, P]
+        L.orc_icp.argtypes = [P, I64, P, P, I64, P, D, I32, D, D, I32, P, P, P, P, P, P, P, P, I32]
         L.orc_voxel_down_sample.restype = I64
         L.orc_voxel_down_sample.argtypes = [P, P, I64, D, P, P]
         L.orc_pass_p2p.argtypes = [P, P, I64, P, I64, P, D, P, P]
@@ -67,7 +69,7 @@ def lib():
         L.orc_estimate_normals.restype = I64
         L.orc_estimate_normals.argtypes = [P, I64, D, I32, P, P]
         L.orc_icp_multiscale.restype = C.c_int
-        L.orc_icp_multiscale.argtypes = [P, I64, P, P, I64, P, I32, P, P, P, D, D, P, P, P, P, P]
+        L.orc_icp_multiscale.argtypes = [P, I64, P, P, I64, P, I32, P, P, P, D, D, P, P, P, P, P, I32]
         _lib = L
     return _lib
 
@@ -121,11 +123,14 @@ def nn(s, target, dmax, grid: Grid | None = None):
     return int(j), float(d2[0])
 
 
-def step(T, source, target, normals, dmax, grid: Grid | None | str = "auto", subset=None):
+def step(T, source, target, normals, dmax, grid: Grid | None | str = "auto", subset=None,
+         threads: int | None = None):
     """One pass at fixed T (icp_step semantics). Returns dict(corr, d2,
     terms[29], abs_terms[29], JTJ (6x6), JTr (6), count, sum_sq_dist).
     ``subset``: optional source indices; corr/d2 then follow that order and
-    the terms sum over the subset only."""
+    the terms sum over the subset only. ``threads``: None = the sequential
+    pass; k >= 1 = the deterministic chunked OpenMP pass on k threads
+    (bitwise the same result for every k)."""
     src, tgt, nrm = _f32(source), _f32(target), _f32(normals)
     if isinstance(grid, str):
         grid = Grid(tgt, dmax) if len(tgt) * len(src) > 4_000_000 else None
@@ -135,9 +140,14 @@ def step(T, source, target, normals, dmax, grid: Grid | None | str = "auto", sub
     d2 = np.empty(k, np.float64)
     sums = np.zeros(NTERMS)
     abss = np.zeros(NTERMS)
-    lib().orc_pass_subset(_p(_f64(T)), _p(src), len(src), _p(idx), k, _p(tgt), _p(nrm), len(tgt),
-                          grid.h if grid is not None else None, float(dmax),
-                          _p(corr), _p(d2), _p(sums), _p(abss))
+    if threads is None:
+        lib().orc_pass_subset(_p(_f64(T)), _p(src), len(src), _p(idx), k, _p(tgt), _p(nrm), len(tgt),
+                              grid.h if grid is not None else None, float(dmax),
+                              _p(corr), _p(d2), _p(sums), _p(abss))
+    elif lib().orc_pass_chunked(_p(_f64(T)), _p(src), len(src), _p(idx), k, _p(tgt), _p(nrm), len(tgt),
+                                grid.h if grid is not None else None, float(dmax),
+                                _p(corr), _p(d2), _p(sums), _p(abss), int(threads)):
+        raise MemoryError("oracle chunked pass failed")
     JTJ = np.zeros(36)
     lib().orc_expand_jtj(_p(sums), _p(JTJ))
     return dict(corr=corr, d2=d2, terms=sums, abs_terms=abss, JTJ=JTJ.reshape(6, 6),
@@ -164,9 +174,10 @@ def compose(A, B):
 
 
 def icp(source, target, normals, dmax, max_iterations, init_T=None, relative_fitness=1e-6,
-        relative_rmse=1e-6, use_grid=True):
+        relative_rmse=1e-6, use_grid=True, threads: int = 0):
     """registration_icp, point-to-plane. Returns dict(T, fitness, inlier_rmse,
-    iterations, flags, converged, passes, hist_fitness, hist_rmse)."""
+    iterations, flags, converged, passes, hist_fitness, hist_rmse).
+    ``threads`` > 0: every pass is the deterministic chunked OpenMP pass."""
     src, tgt, nrm = _f32(source), _f32(target), _f32(normals)
     T0 = _f64(np.eye(4) if init_T is None else init_T)
     T = np.zeros(16)
@@ -177,7 +188,7 @@ def icp(source, target, normals, dmax, max_iterations, init_T=None, relative_fit
     passes = lib().orc_icp(_p(src), len(src), _p(tgt), _p(nrm), len(tgt), _p(T0), float(dmax),
                            int(max_iterations), float(relative_fitness), float(relative_rmse),
                            1 if use_grid else 0, _p(T), _p(fit), _p(rmse), _p(it), _p(fl), _p(cv),
-                           _p(hf), _p(hr))
+                           _p(hf), _p(hr), int(threads))
     if passes < 0:
         raise MemoryError("oracle icp failed")
     return dict(T=T.reshape(4, 4), fitness=float(fit[0]), inlier_rmse=float(rmse[0]),
@@ -199,7 +210,7 @@ def voxel_down_sample(points, voxel, normals=None):
 
 
 def icp_multiscale(source, target, normals, voxels, dmaxs, iters, init_T=None,
-                   relative_fitness=1e-6, relative_rmse=1e-6):
+                   relative_fitness=1e-6, relative_rmse=1e-6, threads: int = 0):
     """Multi-scale point-to-plane ICP (downsample per scale, carry T)."""
     src, tgt, nrm = _f32(source), _f32(target), _f32(normals)
     ns = len(voxels)
@@ -211,7 +222,8 @@ def icp_multiscale(source, target, normals, voxels, dmaxs, iters, init_T=None,
     rc = lib().orc_icp_multiscale(_p(src), len(src), _p(tgt), _p(nrm), len(tgt), _p(T0), ns,
                                   _p(_f64(voxels)), _p(_f64(dmaxs)),
                                   _p(np.ascontiguousarray(iters, np.int32)), float(relative_fitness),
-                                  float(relative_rmse), _p(T), _p(fit), _p(rmse), _p(its), _p(nss))
+                                  float(relative_rmse), _p(T), _p(fit), _p(rmse), _p(its), _p(nss),
+                                  int(threads))
     if rc != 0:
         raise RuntimeError("oracle multiscale failed")
     return dict(T=T.reshape(4, 4), fitness=fit, inlier_rmse=rmse, iterations=its, n_source=nss)

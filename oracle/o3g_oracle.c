@@ -255,6 +255,58 @@ void orc_pass(const double T[16], const float *src, int64_t n, const float *tgt,
     orc_pass_subset(T, src, n, NULL, 0, tgt, nrm, m, g, dmax, corr, NULL, sums, abssums);
 }
 
+/* Deterministic OpenMP mode (SURVEY §8(c) "a fixed chunk partition, with
+ * partials summed in chunk order"; the paper's own parallelisation of the
+ * J^T J / J^T r evaluation, "OpenMP reduction ... for each data record",
+ * P:238-248, Eq. 2). The records are split into fixed chunks of
+ * ORC_CHUNK queries in source order, independent of the thread count; each
+ * chunk is accumulated exactly like orc_pass_subset (Neumaier), and the
+ * chunk partials (their compensated values s + c) are then summed in chunk
+ * order by the same accumulator. The result is therefore bitwise the same
+ * for any nthreads (0/1 = run the chunks on the calling thread). The
+ * correspondences are per-query, hence identical to orc_pass_subset's.   */
+#define ORC_CHUNK 4096
+int orc_pass_chunked(const double T[16], const float *src, int64_t n, const int64_t *idx, int64_t k,
+                     const float *tgt, const float *nrm, int64_t m, const orc_grid *g, double dmax,
+                     int32_t *corr, double *d2out, double *sums, double *abssums, int32_t nthreads)
+{
+    const int64_t cnt = idx ? k : n;
+    const int64_t nch = (cnt + ORC_CHUNK - 1) / ORC_CHUNK;
+    acc_t *part = (acc_t *)calloc((size_t)(nch > 0 ? nch : 1) * ORC_NTERMS, sizeof(acc_t));
+    if (!part) return 1;
+    const double r2 = dmax * dmax;
+    (void)nthreads;
+#pragma omp parallel for schedule(dynamic, 1) num_threads(nthreads > 0 ? nthreads : 1)
+    for (int64_t c = 0; c < nch; ++c) {
+        acc_t *acc = part + c * ORC_NTERMS;
+        const int64_t t1 = (c + 1) * ORC_CHUNK < cnt ? (c + 1) * ORC_CHUNK : cnt;
+        for (int64_t t = c * ORC_CHUNK; t < t1; ++t) {
+            int64_t i = idx ? idx[t] : t;
+            double s[3], d2 = 0.0;
+            orc_transform_point(T, src + 3 * i, s);
+            int64_t j = g ? orc_nn_grid(g, s, r2, &d2) : orc_nn_brute(s, tgt, m, r2, &d2);
+            if (corr) corr[t] = (int32_t)j;
+            if (d2out) d2out[t] = j >= 0 ? d2 : -1.0;
+            if (j >= 0) record(s, tgt + 3 * j, nrm + 3 * j, d2, acc);
+        }
+    }
+    acc_t tot[ORC_NTERMS];
+    memset(tot, 0, sizeof(tot));
+    for (int64_t c = 0; c < nch; ++c)
+        for (int t = 0; t < ORC_NTERMS; ++t) {
+            const acc_t *a = &part[c * ORC_NTERMS + t];
+            double a_abs = tot[t].a + a->a;
+            acc_add(&tot[t], a->s + a->c);
+            tot[t].a = a_abs;   /* sum of |records|, not of |chunk sums| */
+        }
+    for (int t = 0; t < ORC_NTERMS; ++t) {
+        if (sums) sums[t] = tot[t].s + tot[t].c;
+        if (abssums) abssums[t] = tot[t].a;
+    }
+    free(part);
+    return 0;
+}
+
 /* ------------------------------------------------------------------ A8 */
 /* Full symmetric 6x6 from the 21 upper-triangle terms.                  */
 void orc_expand_jtj(const double *terms, double A[36])
@@ -363,7 +415,7 @@ int orc_icp(const float *src, int64_t n, const float *tgt, const float *nrm, int
             const double T0[16], double dmax, int32_t max_iterations, double relative_fitness,
             double relative_rmse, int32_t use_grid, double T_out[16], double *fitness,
             double *inlier_rmse, int32_t *iterations, int32_t *flags, int32_t *converged,
-            double *hist_fit, double *hist_rmse)
+            double *hist_fit, double *hist_rmse, int32_t nthreads)
 {
     orc_grid *g = use_grid ? orc_grid_build(tgt, m, dmax) : NULL;
     if (use_grid && !g) return -1;
@@ -371,7 +423,12 @@ int orc_icp(const float *src, int64_t n, const float *tgt, const float *nrm, int
     memcpy(T, T0, sizeof(T));
     int32_t it = 0, fl = 0, conv = 0, passes = 0;
 
-    orc_pass(T, src, n, tgt, nrm, m, g, dmax, NULL, sums, NULL);
+    /* nthreads > 0: the deterministic chunked (OpenMP) pass */
+#define ORC_PASS()                                                                          \
+    (nthreads > 0 ? (void)orc_pass_chunked(T, src, n, NULL, 0, tgt, nrm, m, g, dmax, NULL, NULL, \
+                                           sums, NULL, nthreads)                            \
+                  : orc_pass(T, src, n, tgt, nrm, m, g, dmax, NULL, sums, NULL))
+    ORC_PASS();
     double cnt = sums[27];
     double fit = cnt / (double)n, rmse = cnt > 0 ? sqrt(sums[28] / cnt) : 0.0;
     if (hist_fit) hist_fit[passes] = fit;
@@ -387,7 +444,7 @@ int orc_icp(const float *src, int64_t n, const float *tgt, const float *nrm, int
         orc_exp_se3(xi, dT);
         orc_compose(dT, T, T);
         ++it;
-        orc_pass(T, src, n, tgt, nrm, m, g, dmax, NULL, sums, NULL);
+        ORC_PASS();
         cnt = sums[27];
         fit = cnt / (double)n;
         rmse = cnt > 0 ? sqrt(sums[28] / cnt) : 0.0;
@@ -406,6 +463,7 @@ int orc_icp(const float *src, int64_t n, const float *tgt, const float *nrm, int
     *flags = fl;
     *converged = conv;
     orc_grid_free(g);
+#undef ORC_PASS
     return passes;
 }
 
@@ -479,7 +537,7 @@ int orc_icp_multiscale(const float *src, int64_t n, const float *tgt, const floa
                        const double T0[16], int32_t nscales, const double *voxel, const double *dmax,
                        const int32_t *iters, double relative_fitness, double relative_rmse,
                        double T_out[16], double *fit_s, double *rmse_s, int32_t *iters_s,
-                       int64_t *nsrc_s)
+                       int64_t *nsrc_s, int32_t nthreads)
 {
     double T[16];
     memcpy(T, T0, sizeof(T));
@@ -494,7 +552,7 @@ int orc_icp_multiscale(const float *src, int64_t n, const float *tgt, const floa
         int32_t it, fl, cv;
         if (ns <= 0 || ms <= 0) { free(sp); free(tp); free(tn); return -1; }
         orc_icp(sp, ns, tp, tn, ms, T, dmax[s], iters[s], relative_fitness, relative_rmse, 1, Tn,
-                &fit, &rmse, &it, &fl, &cv, NULL, NULL);
+                &fit, &rmse, &it, &fl, &cv, NULL, NULL, nthreads);
         memcpy(T, Tn, sizeof(T));
         if (fit_s) fit_s[s] = fit;
         if (rmse_s) rmse_s[s] = rmse;

@@ -9,6 +9,7 @@
 // K4 k_tail: fixed-order sum of the block partials (and, multi-GPU, of the
 //   rank partials in rank order), then fitness / rmse / criteria, the 6x6
 //   LDL^T solve, the SE(3) exponential and T <- exp(xi^) T (A8).
+#include <cuda_fp16.h>
 #include <float.h>
 #include <math_constants.h>
 
@@ -226,8 +227,164 @@ __device__ __forceinline__ int warp_bound_x(const float4* __restrict__ tpos, int
     return lo + __popc(__ballot_sync(0xffffffffu, p < hi && (GE ? x < v : x <= v)));
 }
 
-__device__ __noinline__ void tail_finish(const double* terms, IcpState* st, double* hist_fit, double* hist_rmse,
-                            int mode);
+__device__ __noinline__ void tail_finish(const double* terms, IcpState* st, const TailHist& hist, int mode);
+
+// ------------------------------------------- correspondence certificates
+// A full search at pass b of the query point P_b = T_b s
+// (fp64, fixed order) leaves a certificate rho: with U1 an upper bound on the
+// true distance |P_b - q_w| of the winner and L2 a lower bound on the true
+// distance to every other target, rho = (L2 - U1) / 2; with no winner, L1 a
+// lower bound on the distance to every target, rho = L1 - dmax (+ margins).
+// At a later pass k, if the computed points moved by eps = |P_k - P_b| < rho
+// then (triangle inequality) the winner is strictly nearer than every other
+// target, so it is again the unique minimum of the fp64 d^2 (relative error
+// < 2^-50, covered by 2^-40 margins) and the pass's answer is w iff
+// d2_64(P_k, w) <= r^2 (R1-R3); with no winner every target stays beyond dmax.
+// eps is bounded in fp32 from dT = T_k - T_b (smem, per age) with a rigorous
+// rounding term c_age. All bounds below round outward.
+__device__ __forceinline__ float sqrt_approx(float x) {
+    float r;
+    asm("sqrt.approx.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+__device__ __forceinline__ float sqrt_lo(float x) { return __fmul_rd(sqrt_approx(x), 1.0f - 1.52587890625e-05f); }
+__device__ __forceinline__ float sqrt_hi(float x) {
+    return __fadd_ru(__fmul_ru(sqrt_approx(x), 1.0f + 1.52587890625e-05f), 2e-19f);
+}
+// lower bound on |q - P| from a prefilter value df = fl32(|q - fl32(P)|^2)
+// (df <= |q - sh|^2 (1 + 2^-24)^5, |sh - P| <= E1)
+__device__ __forceinline__ float lo_from_df(float df, float E1u) {
+    return __fsub_rd(sqrt_lo(df), E1u);
+}
+// smallest distance from (x, y, z) in cell (cx, cy, cz) to that cell's 6 faces
+// (rounded down, face_gaps margins): a target outside the 27-cell stencil is
+// at >= h + this
+__device__ __forceinline__ float min_face_gap(const GridDev& g, double x, double y, double z, int cx, int cy,
+                                              int cz) {
+    float g0, g1, g2, g3, g4, g5;
+    face_gaps(x, g.ox, g.h, cx, g0, g1);
+    face_gaps(y, g.oy, g.h, cy, g2, g3);
+    face_gaps(z, g.oz, g.h, cz, g4, g5);
+    return fminf(fminf(fminf(g0, g1), fminf(g2, g3)), fminf(g4, g5));
+}
+// The same bound from t = (x - o) inv_h, the fp64 cell coordinate before
+// flooring (cell_coord's intermediate): the gaps are (t - c) h and (c + 1 - t) h;
+// t carries a relative error < 2^-50 (and so does every target's cell
+// assignment), covered by the margin 2^-46 (|t| + 1). A clamped cell gives 0.
+__device__ __forceinline__ float min_face_gap_t(const GridDev& g, const double t[3], const int c[3]) {
+    double m = 1.0;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const double f = __dsub_rn(t[k], (double)c[k]);
+        const double e = 1.4210854715202004e-14 * (fabs(t[k]) + 1.0);   // 2^-46 (|t| + 1)
+        m = fmin(m, fmin(f, 1.0 - f) - e);
+    }
+    return m > 0.0 ? __double2float_rd(m * g.h * (1.0 - 1e-15)) : 0.f;
+}
+
+// a squared-distance bound u widened to (sqrt(u) + 2 rg)^2, rounded up
+__device__ __forceinline__ float widen_ub(float u, float rg) {
+    const float t = __fadd_ru(sqrt_hi(u), __fmul_ru(2.0f, rg));
+    return __fmul_ru(t, t);
+}
+__device__ __forceinline__ unsigned cert_pack(int pass, float rho, float inv_h_rd) {
+    if (!(rho > 0.f)) return 0xFFFFFFFFu;
+    const __half q = __float2half_rz(__fmul_rd(rho, inv_h_rd));   // <= rho / h
+    return ((unsigned)pass << 16) | (unsigned)__half_as_ushort(q);
+}
+__device__ __forceinline__ bool cert_valid(unsigned pk, int pass, float x, float y, float z,
+                                           const float4 (*dT)[3], const float* dC, float h_rd) {
+    const int bp = (int)(pk >> 16), age = pass - bp;
+    if (bp == 0xFFFF || age < 1 || age > kCertAges) return false;
+    const float4 d0 = dT[age - 1][0], d1 = dT[age - 1][1], d2 = dT[age - 1][2];
+    const float ex = fmaf(d0.z, z, fmaf(d0.y, y, fmaf(d0.x, x, d0.w)));
+    const float ey = fmaf(d1.z, z, fmaf(d1.y, y, fmaf(d1.x, x, d1.w)));
+    const float ez = fmaf(d2.z, z, fmaf(d2.y, y, fmaf(d2.x, x, d2.w)));
+    const float e2 = fmaf(ez, ez, fmaf(ey, ey, ex * ex));
+    const float rho = __fmul_rd(__half2float(__ushort_as_half((unsigned short)(pk & 0xFFFFu))), h_rd);
+    const float thr = __fmul_rd(__fsub_rd(rho, dC[age - 1]), 1.0f - 9.5367431640625e-07f);
+    return thr > 0.f && __fmul_ru(e2, 1.0f + 1.9073486328125e-06f) < __fmul_rd(thr, thr);
+}
+
+// Certificate tables of a block (one thread per age 1..kCertAges): dT = T_pass -
+// T_(pass-age) in fp32 and the rounding bound c_age of the fp32 displacement
+// |dT (s,1)| (see cert_valid): |dT32 (s,1) - (P_pass - P_b)| <= 2^-20 sum_rk
+// |dT_rk| smax_k (dT rounding + three fp32 FMAs) + 2^-48 max(sum |T_rk| smax_k)
+// (the fp64 transforms). Age 1 also sets the search goal rho_g: searches stage
+// rows up to (previous winner's distance + 2 rho_g), rho_g = 4 x (a bound on the
+// last pass's largest displacement), capped at h, so their certificates can
+// outlive ~4 such passes.
+__device__ __forceinline__ void cert_tables(const K3Args& a, int pass, int age, float4 (*sDT)[3], float* sDC,
+                                            float* s_rhog) {
+    float c = CUDART_INF_F;   // (no such pass: never valid)
+    if (age <= pass) {
+        const double* Tb = a.hist_Tr + 16 * (size_t)(pass - age);
+        double S = 0.0, M = 0.0;
+#pragma unroll
+        for (int r = 0; r < 3; ++r) {
+            double Sr = 0.0, Mp = 0.0, Mb = 0.0;
+            float dv[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const double tp = a.st->T[4 * r + k], tb = Tb[4 * r + k], d = tp - tb;
+                const double sm = k < 3 ? (double)a.smax[k] : 1.0;
+                dv[k] = (float)d;
+                Sr += fabs(d) * sm, Mp += fabs(tp) * sm, Mb += fabs(tb) * sm;
+            }
+            sDT[age - 1][r] = make_float4(dv[0], dv[1], dv[2], dv[3]);
+            S += Sr, M += fmax(Mp, Mb);
+        }
+        c = __double2float_ru((S * 9.5367431640625e-07 + M * 3.552713678800501e-15) * (1.0 + 1e-6));
+        if (age == 1) *s_rhog = (float)fmin(a.rhog_mul * S, a.rhog_cap * a.g.h);
+    }
+    if (age == 1 && pass == 0) *s_rhog = (float)(a.rhog_cap * a.g.h);
+    sDC[age - 1] = c;
+}
+
+// A5 + A6 for the warp's current records: r = (s'-q).n, J = [s' x n ; n] (R4)
+// -> V = (J, r, m), W = (J, m, d2); C += V^T W on the fp64 tensor cores,
+// 4 records per mma, fixed order (point-to-point: the (s', q) record)
+__device__ __forceinline__ void accumulate_records(const K3Args& a, double* vw, int lane, int win, double sx,
+                                                   double sy, double sz, float4 wq, float4 nf, double wd2,
+                                                   double& acc0, double& acc1) {
+    const unsigned matched = __ballot_sync(0xffffffffu, win >= 0);
+    if (!matched) return;
+    double v[8] = {0, 0, 0, 0, 0, 0, 0, 0}, d2w = 0.0;
+    if (win >= 0 && a.p2p) {
+        // point-to-point record, staged as rows 0-3 (s', 1) and 4-6 (q)
+        v[0] = sx, v[1] = sy, v[2] = sz, v[3] = 1.0;
+        v[4] = wq.x, v[5] = wq.y, v[6] = wq.z;
+        v[7] = 0.0;
+        d2w = wd2;
+    } else if (win >= 0) {
+        const double nx = nf.x, ny = nf.y, nz = nf.z;
+        v[0] = sy * nz - sz * ny;
+        v[1] = sz * nx - sx * nz;
+        v[2] = sx * ny - sy * nx;
+        v[3] = nx, v[4] = ny, v[5] = nz;
+        v[6] = (sx - (double)wq.x) * nx + (sy - (double)wq.y) * ny + (sz - (double)wq.z) * nz;
+        v[7] = 1.0;
+        d2w = wd2;
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) vw[q * kVW + lane] = v[q];
+    vw[8 * kVW + lane] = d2w;
+    __syncwarp();
+    // plane: V rows (J0..J5, r, m) = 0..7; W rows (J0..J5, m, d2) = 0..5, 7, 8.
+    // point: V = (s'x, s'y, s'z, 1, 0..) = rows 0-3 then zero row 7;
+    //        W = (qx, qy, qz, 1, d2, 0..) = rows 4, 5, 6, 3, 8 then row 7, so
+    //        C[a][b] = sum s'_a q_b, C[a][3] = sum s'_a, C[3][b] = sum q_b,
+    //        C[3][3] = count, C[3][4] = sum d2 (term_cidx_p2p)
+    const int row = lane >> 2, kk = lane & 3;
+    const int wrow = a.p2p ? (row < 3 ? row + 4 : row == 3 ? 3 : row == 4 ? 8 : 7) : (row < 6 ? row : row + 1);
+    const int vrow = a.p2p ? (row < 4 ? row : 7) : row;
+#pragma unroll
+    for (int c4 = 0; c4 < 8; ++c4) {
+        if ((matched >> (4 * c4)) & 0xFu)
+            dmma884(acc0, acc1, vw[vrow * kVW + 4 * c4 + kk], vw[wrow * kVW + 4 * c4 + kk]);
+    }
+    __syncwarp();
+}
 
 // live test of the query in cell (cx, cy, cz) (cells in [-2, n+1]): one bit
 // of the dilated occupancy bitmap — per cell on a dense grid; on a hashed grid
@@ -251,9 +408,20 @@ template <bool WRITE_CORR, bool COOP, bool PRUNE>
 __global__ void __launch_bounds__(kK3Threads, 4) k3_balanced(const K3Args a) {
     extern __shared__ __align__(16) unsigned char k3smem[];
     __shared__ double sT[12];
+    __shared__ __align__(16) float4 sDT[kCertAges][3];   // (certificates: cert_tables)
+    __shared__ float sDC[kCertAges];
+    __shared__ float s_rhog;
     if (!a.eval_T && a.st->done) return;
+    // certificates: a.cert set (the run loop) and this pass in certificate mode
+    // (the warm-start seed is prev_j in both modes)
+    const bool certm = a.cert != nullptr && !a.eval_T && a.st->cmode;
+    const uint8_t* need = certm ? a.need : nullptr;
+    const int pass = certm ? a.st->passes : 0;
     if (threadIdx.x < 12) sT[threadIdx.x] = a.eval_T ? a.eval_T[16 * blockIdx.y + threadIdx.x] : a.st->T[threadIdx.x];
+    if (certm && threadIdx.x >= 32 && threadIdx.x < 32 + kCertAges)
+        cert_tables(a, pass, threadIdx.x - 31, sDT, sDC, &s_rhog);
     __syncthreads();
+    const float rhog = certm ? s_rhog : 0.f;
 
     const GridDev g = a.g;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -278,16 +446,63 @@ __global__ void __launch_bounds__(kK3Threads, 4) k3_balanced(const K3Args a) {
     // skipped (measured: large16m queue 0.650 vs 0.733 ms at T_init (fitness
     // 0.36), 1.145 vs 1.039 ms converged; fragment (fitness 0.55) step 11.01
     // -> 10.64 ms with 0.5 instead of 0.7). Results are the same either way.
-    const bool use_queue = a.nbr_bits != nullptr && !(!a.eval_T && a.st->passes > 0 && a.st->fit > 0.5);
+    // (with certificates the pre-pass also settles the certified queries: always on)
+    const bool use_queue = need != nullptr || (a.nbr_bits != nullptr && !(!a.eval_T && a.st->passes > 0 && a.st->fit > 0.5));
     const bool warm = a.prev_j && !a.eval_T && a.st->passes > 0;
+    const float Lout = __fmul_rd(a.h_rd, 1.0f - 1.1920928955078125e-07f);   // stencil reach >= h (§5.1 margins)
+    const float dmax_hi = __double2float_ru(a.dmax * (1.0 + 9.094947017729282e-13));
     __shared__ float4 s_gap[PRUNE && COOP ? kK3Threads / 32 : 1][32];
     __shared__ int s_rmask[PRUNE && COOP ? kK3Threads / 32 : 1][32];
     __shared__ float s_uw[PRUNE && COOP ? kK3Threads / 32 : 1][32];   // warm bound per query
     int qn = 0;   // warp-uniform queue length
-    int base = gw * 32;
+    // flag mode (after k3_sweep): the warp walks chunks of kChunk consecutive
+    // queries (chunk gw, gw + nw, ...), so its queue holds spatially close queries
+    constexpr int kChunk = 256;
+    int base = (need && !a.ilv) ? gw * kChunk : gw * 32;
+    // (flag mode) the current chunk's 256 flags, 8 per lane, and its next sub-batch
+    unsigned long long cw = 0ull, pf = 0ull;
+    int cj = 8, cbase = 0, pf_base = a.n;
+    const bool chunked = need && !a.ilv;
+    if (chunked) {   // prime the one-chunk-ahead flag prefetch
+        pf_base = base;
+        base += nw * kChunk;
+        pf = pf_base + 8 * lane < a.n ? __ldg((const unsigned long long*)(need + pf_base + 8 * lane)) : 0ull;
+    }
+    int nsearch = 0, ncand = 0;   // this lane's full searches and their candidates (statistics)
+    __shared__ int s_stat[kK3Threads / 32][2];
     for (;;) {
         int i;
         if (use_queue) {
+          if (chunked) {
+            // flag mode: one 8-byte load per lane covers a chunk of 256 queries;
+            // chunks whose flags are all zero are skipped with one ballot
+            while (qn < 32) {
+                if (cj == 8) {
+                    // next chunk with a flag; the following chunk's flags are
+                    // already in flight (pf, loaded one chunk ahead)
+                    bool found = false;
+                    while (pf_base < a.n) {
+                        cbase = pf_base;
+                        cw = pf;
+                        pf_base = base;
+                        base += nw * kChunk;
+                        pf = pf_base + 8 * lane < a.n ? __ldg((const unsigned long long*)(need + pf_base + 8 * lane)) : 0ull;
+                        if (__ballot_sync(0xffffffffu, cw != 0ull)) { found = true; break; }
+                    }
+                    if (!found) break;
+                    cj = 0;
+                }
+                const int q = 32 * cj + lane;
+                const unsigned long long ww = __shfl_sync(0xffffffffu, cw, q >> 3);
+                const bool live = ((ww >> (8 * (q & 7))) & 0xffull) != 0ull;
+                const int i0 = cbase + q;
+                ++cj;
+                const unsigned lb = __ballot_sync(0xffffffffu, live);
+                if (live) qbuf[warp][qn + __popc(lb & ((1u << lane) - 1u))] = i0;
+                qn += __popc(lb);
+                __syncwarp();
+            }
+          } else {
         while (qn < 32 && base < a.n) {
             // interleaved batches (a.ilv = number of batches): lane l of batch b
             // takes query l * ilv + b, so queries that cluster in the ordered
@@ -295,9 +510,11 @@ __global__ void __launch_bounds__(kK3Threads, 4) k3_balanced(const K3Args a) {
             const int i0 = a.ilv ? min(lane * a.ilv + (base >> 5), a.n) : base + lane;
             base += nw * 32;
             // the warp's next source batch: in flight while this one is processed
-            if (!a.ilv && base + lane < a.n) asm volatile("prefetch.global.L1 [%0];" ::"l"(a.src + base + lane));
+            if (!a.ilv && !need && base + lane < a.n) asm volatile("prefetch.global.L1 [%0];" ::"l"(a.src + base + lane));
             bool live = false;
-            if (i0 < a.n) {
+            if (i0 < a.n && need) {
+                live = __ldg(&need[i0]) != 0;   // (k3_sweep settled every other query)
+            } else if (i0 < a.n) {
                 const float4 p0 = __ldg(&a.src[i0]);
                 double tx, ty, tz;
                 xform_rn(sT, p0.x, p0.y, p0.z, tx, ty, tz);
@@ -321,6 +538,7 @@ __global__ void __launch_bounds__(kK3Threads, 4) k3_balanced(const K3Args a) {
             qn += __popc(lb);
             __syncwarp();
         }
+          }
         if (qn == 0) break;
         const int take = min(qn, 32);
         i = lane < take ? qbuf[warp][lane] : a.n;
@@ -345,9 +563,13 @@ __global__ void __launch_bounds__(kK3Threads, 4) k3_balanced(const K3Args a) {
         float gym = 0.f, gyp = 0.f, gzm = 0.f, gzp = 0.f;
         int rmask = 0;
         float4 p = make_float4(0.f, 0.f, 0.f, 0.f);
+        // (certificates) lower bound on d^2 over the stencil rows / cells that were
+        // not staged (each was dropped by a bound L > ub on its squared distance)
+        float Lskip = CUDART_INF_F;
         if (i < a.n) {
             p = __ldg(&a.src[i]);
-            const int jprev = warm ? __ldg(&a.prev_j[i]) : -1;   // previous pass's winner (warm start)
+            // previous winner (warm start): the prior pass's, or the certificate's
+            const int jprev = warm ? __ldg(&a.prev_j[i]) : -1;   // previous winner (warm start)
             xform_rn(sT, p.x, p.y, p.z, sx, sy, sz);
             const int cx = cell_coord(sx, g.ox, g.inv_h, g.nx);
             const int cy = cell_coord(sy, g.oy, g.inv_h, g.ny);
@@ -391,17 +613,22 @@ __global__ void __launch_bounds__(kK3Threads, 4) k3_balanced(const K3Args a) {
                             const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)),
                                                         __dmul_rn(dz, dz));
                             ub = __double2float_ru(d2 * (1.0 + 9.094947017729282e-13));   // (1 + 2^-40), up
+                            if (certm) ub = widen_ub(ub, rhog);   // (certificate goal)
                             face_gaps(sy, g.oy, g.h, cy, gym, gyp);
                             face_gaps(sz, g.oz, g.h, cz, gzm, gzp);
                         }
                     }
 #pragma unroll
                     for (int r = 0; r < 9; ++r) {
-                        if (ee[r] > bb[r] &&
-                            (r == 4 || !(row_lower(r % 3 - 1, r / 3 - 1, gym, gyp, gzm, gzp) > ub))) {
-                            segs[nseg * 32 + lane] = make_int2(bb[r], ee[r]);
-                            ++nseg;
-                            c += ee[r] - bb[r];
+                        if (ee[r] > bb[r]) {
+                            const float Lr = row_lower(r % 3 - 1, r / 3 - 1, gym, gyp, gzm, gzp);
+                            if (r == 4 || !(Lr > ub)) {
+                                segs[nseg * 32 + lane] = make_int2(bb[r], ee[r]);
+                                ++nseg;
+                                c += ee[r] - bb[r];
+                            } else {
+                                Lskip = fminf(Lskip, Lr);
+                            }
                         }
                     }
                 } else {
@@ -434,6 +661,7 @@ __global__ void __launch_bounds__(kK3Threads, 4) k3_balanced(const K3Args a) {
                             const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)),
                                                         __dmul_rn(dz, dz));
                             uw = __double2float_ru(d2 * (1.0 + 9.094947017729282e-13));
+                            if (certm) uw = widen_ub(uw, rhog);
                         }
                     }
                     if (tot >= a.prune_min || (COOP && tot >= a.coop_min) || uw < CUDART_INF_F) {
@@ -470,15 +698,21 @@ __global__ void __launch_bounds__(kK3Threads, 4) k3_balanced(const K3Args a) {
 #pragma unroll
                     for (int t = 0; t < 9; ++t) {
                         const int r = kOrder[t];
-                        if (ee[r] > bb[r] && ((k0 == 1 && nseg == 0) || ub == CUDART_INF_F ||
-                                              !(row_lower(r % 3 - 1, r / 3 - 1, gym, gyp, gzm, gzp) > ub))) {
+                        if (ee[r] <= bb[r]) continue;
+                        const float Lr = row_lower(r % 3 - 1, r / 3 - 1, gym, gyp, gzm, gzp);
+                        if ((k0 == 1 && nseg == 0) || ub == CUDART_INF_F || !(Lr > ub)) {
                             int b = bb[r], e = ee[r];
                             if (uw < CUDART_INF_F && w == 3) {
                                 // warm: an end cell (cx -+ 1) with L_row + gx^2 > ub is cut
-                                const float Lr = row_lower(r % 3 - 1, r / 3 - 1, gym, gyp, gzm, gzp);
                                 const int rb = rb0 + (r / 3) * nxny + (r % 3) * g.nx;
-                                if (__fadd_rd(Lr, gxm2) > ub) b = __ldg(cs + rb + 1);
-                                if (__fadd_rd(Lr, gxp2) > ub) e = __ldg(cs + rb + 2);
+                                if (__fadd_rd(Lr, gxm2) > ub) {
+                                    b = __ldg(cs + rb + 1);
+                                    if (b > bb[r]) Lskip = fminf(Lskip, __fadd_rd(Lr, gxm2));
+                                }
+                                if (__fadd_rd(Lr, gxp2) > ub) {
+                                    e = __ldg(cs + rb + 2);
+                                    if (e < ee[r]) Lskip = fminf(Lskip, __fadd_rd(Lr, gxp2));
+                                }
                             }
                             if (e > b) {
                                 segs[nseg * 32 + lane] = make_int2(b, e);
@@ -486,6 +720,8 @@ __global__ void __launch_bounds__(kK3Threads, 4) k3_balanced(const K3Args a) {
                                 c += e - b;
                                 rmask |= 1 << t;
                             }
+                        } else {
+                            Lskip = fminf(Lskip, Lr);
                         }
                     }
                     if (COOP) {
@@ -504,12 +740,19 @@ __global__ void __launch_bounds__(kK3Threads, 4) k3_balanced(const K3Args a) {
                                  dz = __dsub_rn(sz, (double)t.z);
                     const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
                     ub = __double2float_ru(d2 * (1.0 + 9.094947017729282e-13));
+                    if (certm) ub = widen_ub(ub, rhog);
                     face_gaps(sy, g.oy, g.h, cy, hym, hyp);
                     face_gaps(sz, g.oz, g.h, cz, hzm, hzp);
                 }
                 for (int z = zlo; z <= zhi; ++z) {
                     for (int y = ylo; y <= yhi; ++y) {
-                        if (ub < CUDART_INF_F && row_lower(y - cy, z - cz, hym, hyp, hzm, hzp) > ub) continue;
+                        if (ub < CUDART_INF_F) {
+                            const float Lr = row_lower(y - cy, z - cz, hym, hyp, hzm, hzp);
+                            if (Lr > ub) {   // (an empty row also lands here: a valid bound)
+                                Lskip = fminf(Lskip, Lr);
+                                continue;
+                            }
+                        }
                         int b0, e0, b1 = 0, e1 = 0;
                         if (!g.hashed) {
                             const int rb = (z * g.ny + y) * g.nx;   // < table_size < 2^31
@@ -547,6 +790,7 @@ __global__ void __launch_bounds__(kK3Threads, 4) k3_balanced(const K3Args a) {
         int win = -1, widx = -1;
         double wd2 = 0.0;
         float4 wq = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (i < a.n) ++nsearch, ncand += c;
 
         // heavy queries (>= coop_min candidates, e.g. LiDAR near the sensor): the
         // whole warp scans one query at a time with coalesced lane-strided loads,
@@ -732,6 +976,7 @@ __global__ void __launch_bounds__(kK3Threads, 4) k3_balanced(const K3Args a) {
         }
 
         // decision (exact fp64 rule, R1-R3)
+        bool uniq = !heavy;   // (certificates: the decision had a unique nearest candidate)
         if (!heavy && c > 0 && m1 <= thr0) {
             const float4 t = __ldg(&a.tpos[j1]);
             const double dx = __dsub_rn(sx, (double)t.x), dy = __dsub_rn(sy, (double)t.y),
@@ -742,6 +987,7 @@ __global__ void __launch_bounds__(kK3Threads, 4) k3_balanced(const K3Args a) {
                 if (d2 <= r2) { win = j1, widx = __float_as_int(t.w), wd2 = d2, wq = t; }
             } else {
                 // near-tie (or duplicate visit): exact filtered rescan
+                uniq = false;
                 double bd = CUDART_INF;
                 int bidx = INT_MAX;
                 float thr = thr0;
@@ -766,53 +1012,49 @@ __global__ void __launch_bounds__(kK3Threads, 4) k3_balanced(const K3Args a) {
             }
         }
         if (WRITE_CORR && i < a.n) a.corr_out[__float_as_int(p.w)] = widx;
-        if (a.prev_j && i < a.n) a.prev_j[i] = win;   // the next pass's warm start
-
-        // A5: r = (s'-q).n, J = [s' x n ; n] (R4) -> V = (J, r, m), W = (J, m, d2)
-        const unsigned matched = __ballot_sync(0xffffffffu, win >= 0);
-        if (matched) {
-            double v[8] = {0, 0, 0, 0, 0, 0, 0, 0}, d2w = 0.0;
-            if (win >= 0 && a.p2p) {
-                // point-to-point record, staged as rows 0-3 (s', 1) and 4-6 (q)
-                v[0] = sx, v[1] = sy, v[2] = sz, v[3] = 1.0;
-                v[4] = wq.x, v[5] = wq.y, v[6] = wq.z;
-                v[7] = 0.0;
-                d2w = wd2;
-            } else if (win >= 0) {
-                const float4 nf = __ldg(&a.tnrm[win]);
-                const double nx = nf.x, ny = nf.y, nz = nf.z;
-                v[0] = sy * nz - sz * ny;
-                v[1] = sz * nx - sx * nz;
-                v[2] = sx * ny - sy * nx;
-                v[3] = nx, v[4] = ny, v[5] = nz;
-                v[6] = (sx - (double)wq.x) * nx + (sy - (double)wq.y) * ny + (sz - (double)wq.z) * nz;
-                v[7] = 1.0;
-                d2w = wd2;
+        float4 wn = make_float4(0.f, 0.f, 0.f, 0.f);   // the winner's normal (plane records)
+        if (win >= 0 && !a.p2p) wn = __ldg(&a.tnrm[win]);
+        if (certm && i < a.n) {
+            // certificate of this search: every target other than the winner is at
+            // >= L2 (scanned candidates by their prefilter values, unstaged rows /
+            // cells by their bounds, the rest of the grid beyond the stencil's
+            // outer faces, >= h + the own cell's smallest face gap); rho =
+            // (L2 - U1) / 2, or L1 - dmax with no winner
+            float rho = 0.f;
+            if (uniq) {
+                const float E1u = __double2float_ru(E1);
+                const double tc[3] = {__dmul_rn(__dsub_rn(sx, g.ox), g.inv_h), __dmul_rn(__dsub_rn(sy, g.oy), g.inv_h),
+                                      __dmul_rn(__dsub_rn(sz, g.oz), g.inv_h)};
+                const int cc[3] = {min(max(__double2int_rd(tc[0]), -2), g.nx + 1),
+                                   min(max(__double2int_rd(tc[1]), -2), g.ny + 1),
+                                   min(max(__double2int_rd(tc[2]), -2), g.nz + 1)};
+                float L = fminf(__fadd_rd(Lout, min_face_gap_t(g, tc, cc)), sqrt_lo(Lskip));
+                if (win >= 0) {
+                    L = fminf(L, lo_from_df(m2, E1u));
+                    const float U1 = sqrt_hi(__double2float_ru(wd2 * (1.0 + 9.094947017729282e-13)));
+                    rho = __fmul_rd(__fsub_rd(L, U1), 0.5f);
+                } else {
+                    L = fminf(L, lo_from_df(m1, E1u));
+                    rho = __fsub_rd(L, dmax_hi);
+                }
             }
-#pragma unroll
-            for (int q = 0; q < 8; ++q) vw[q * kVW + lane] = v[q];
-            vw[8 * kVW + lane] = d2w;
-            __syncwarp();
-            // A6: C += V^T W over the 32 records, 4 records per mma (fixed order)
-            // plane: V rows (J0..J5, r, m) = 0..7; W rows (J0..J5, m, d2) = 0..5, 7, 8.
-            // point: V = (s'x, s'y, s'z, 1, 0..) = rows 0-3 then zero row 7;
-            //        W = (qx, qy, qz, 1, d2, 0..) = rows 4, 5, 6, 3, 8 then row 7, so
-            //        C[a][b] = sum s'_a q_b, C[a][3] = sum s'_a, C[3][b] = sum q_b,
-            //        C[3][3] = count, C[3][4] = sum d2 (term_cidx_p2p)
-            const int row = lane >> 2, kk = lane & 3;
-            const int wrow = a.p2p ? (row < 3 ? row + 4 : row == 3 ? 3 : row == 4 ? 8 : 7)
-                                   : (row < 6 ? row : row + 1);
-            const int vrow = a.p2p ? (row < 4 ? row : 7) : row;
-#pragma unroll
-            for (int c4 = 0; c4 < 8; ++c4) {
-                if ((matched >> (4 * c4)) & 0xFu)
-                    dmma884(acc0, acc1, vw[vrow * kVW + 4 * c4 + kk], vw[wrow * kVW + 4 * c4 + kk]);
-            }
-            __syncwarp();
+            a.cert[2 * (size_t)i] = make_float4(__int_as_float(win), __uint_as_float(cert_pack(pass, rho, a.inv_h_rd)), wq.x, wq.y);
+            if (win >= 0) a.cert[2 * (size_t)i + 1] = make_float4(wq.z, wn.x, wn.y, wn.z);
         }
+        if (a.prev_j && i < a.n) {
+            a.prev_j[i] = win;   // the next pass's warm start
+        }
+
+        accumulate_records(a, vw, lane, win, sx, sy, sz, wq, wn, wd2, acc0, acc1);
     }
 
     __syncwarp();
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        nsearch += __shfl_xor_sync(0xffffffffu, nsearch, o);
+        ncand += __shfl_xor_sync(0xffffffffu, ncand, o);
+    }
+    if (lane == 0) s_stat[warp][0] = nsearch, s_stat[warp][1] = ncand;
     vw[(lane >> 2) * 8 + 2 * (lane & 3)] = acc0;   // C of this warp, on its own staging bytes
     vw[(lane >> 2) * 8 + 2 * (lane & 3) + 1] = acc1;
     __syncthreads();
@@ -823,7 +1065,9 @@ __global__ void __launch_bounds__(kK3Threads, 4) k3_balanced(const K3Args a) {
         if (ci >= 0)
             for (int w = 0; w < kK3Threads / 32; ++w)
                 s += ((const double*)(k3smem + (size_t)w * k3v2_warp_bytes(g.hashed)))[ci];
-        a.block_partials[((size_t)blockIdx.y * gridDim.x + blockIdx.x) * kTermStride + threadIdx.x] = s;
+        if (threadIdx.x == kStatSearched || threadIdx.x == kStatCandidates)
+            for (int w = 0; w < kK3Threads / 32; ++w) s += (double)s_stat[w][threadIdx.x - kStatSearched];
+        a.block_partials[((size_t)blockIdx.y * gridDim.x + a.part_off + blockIdx.x) * kTermStride + threadIdx.x] = s;
     }
     if (!a.fuse_mode) return;
 
@@ -838,18 +1082,249 @@ __global__ void __launch_bounds__(kK3Threads, 4) k3_balanced(const K3Args a) {
     __syncthreads();
     if (!s_last) return;
     __threadfence();
-    for (int t = warp; t < kTerms; t += kK3Threads / 32) {
+    // (fixed order: lane t = term t; warp w sums the partials b = w (mod 8) in
+    // four interleaved chains, combined in a fixed order, then the 8 warps in
+    // warp order; every load is a coalesced 256-byte partial row)
+    {
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+        constexpr int W = kK3Threads / 32;
+        int b = warp;
+        for (; b + 3 * W < a.part_total; b += 4 * W) {
+            s0 += __ldcg(&a.block_partials[(size_t)b * kTermStride + lane]);
+            s1 += __ldcg(&a.block_partials[(size_t)(b + W) * kTermStride + lane]);
+            s2 += __ldcg(&a.block_partials[(size_t)(b + 2 * W) * kTermStride + lane]);
+            s3 += __ldcg(&a.block_partials[(size_t)(b + 3 * W) * kTermStride + lane]);
+        }
+        for (; b < a.part_total; b += W) s0 += __ldcg(&a.block_partials[(size_t)b * kTermStride + lane]);
+        vw[lane] = (s0 + s1) + (s2 + s3);   // (this warp's staging bytes are free here)
+    }
+    __syncthreads();
+    if (threadIdx.x < kTermsStats) {
         double s = 0.0;
-        for (int b = lane; b < (int)gridDim.x; b += 32) s += __ldcg(&a.block_partials[(size_t)b * kTermStride + t]);
-#pragma unroll
-        for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-        if (lane == 0) terms[t] = s;
+        for (int w = 0; w < kK3Threads / 32; ++w)
+            s += ((const double*)(k3smem + (size_t)w * k3v2_warp_bytes(g.hashed)))[threadIdx.x];
+        terms[threadIdx.x] = s;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
         *a.counter = 0u;
-        tail_finish(terms, a.st_rw, a.hist_fit, a.hist_rmse, a.fuse_mode);
+        tail_finish(terms, a.st_rw, TailHist{a.hist_fit, a.hist_rmse, a.hist_T, a.hist_terms}, a.fuse_mode);
     }
+}
+
+// ------------------------------------------------ K3a: certificate sweep
+// (run loop with certificates) One streaming pass over the
+// local queries, 32 consecutive per warp batch and two batches in flight per
+// warp (their source records and 32-byte certificates are loaded before either
+// is processed). A query with a valid certificate is settled here: its cached
+// winner decides by this pass's exact d^2 (R1) and its record joins the warp's
+// V^T W contraction (A5/A6). An expired one is transformed (A3) and tested
+// against the dilated occupancy bitmap: dead (empty 27-cell stencil) -> a
+// fresh certificate and no record; live -> need[i] = 1, searched by
+// k3_balanced. Deterministic: fixed batches, fixed mma order, one partial per
+// block.
+constexpr int kSweepThreads = 256;
+
+__device__ __forceinline__ void ld_cert(const float4* c, float4& x, float4& y) {
+    asm volatile("ld.global.nc.L1::no_allocate.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=f"(x.x), "=f"(x.y), "=f"(x.z), "=f"(x.w), "=f"(y.x), "=f"(y.y), "=f"(y.z), "=f"(y.w)
+                 : "l"(c));
+}
+
+template <bool WRITE_CORR>
+__device__ __forceinline__ int sweep_query(const K3Args& a, const GridDev& g, const double* sT,
+                                            const float4 (*sDT)[3], const float* sDC, int pass, int i, float4 p,
+                                            float4 ca, float4 cb, float Lout, float dmax_hi, double* vw, int lane,
+                                            double& acc0, double& acc1) {
+    int cwin = -1;
+    bool certified = false;
+    double tx = 0.0, ty = 0.0, tz = 0.0, cd2 = 0.0;
+    float4 cq = make_float4(0.f, 0.f, 0.f, 0.f), cn = cq;
+    if (i < a.n) {
+        const bool cv = cert_valid(__float_as_uint(ca.y), pass, p.x, p.y, p.z, sDT, sDC, a.h_rd);
+        const int cj = __float_as_int(ca.x);
+        bool need = false;
+        if (!cv || cj >= 0) xform_rn(sT, p.x, p.y, p.z, tx, ty, tz);
+        if (cv) {
+            if (cj >= 0) {
+                const double dx = __dsub_rn(tx, (double)ca.z), dy = __dsub_rn(ty, (double)ca.w),
+                             dz = __dsub_rn(tz, (double)cb.x);
+                const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+                if (d2 <= a.r2) {
+                    cwin = cj, cd2 = d2;
+                    cq = make_float4(ca.z, ca.w, cb.x, 0.f);
+                    cn = make_float4(cb.y, cb.z, cb.w, 0.f);
+                }
+            }
+            if (WRITE_CORR) a.corr_out[__float_as_int(p.w)] = cwin >= 0 ? __float_as_int(__ldg(&a.tpos[cwin].w)) : -1;
+        } else {
+            const double tc[3] = {__dmul_rn(__dsub_rn(tx, g.ox), g.inv_h), __dmul_rn(__dsub_rn(ty, g.oy), g.inv_h),
+                                  __dmul_rn(__dsub_rn(tz, g.oz), g.inv_h)};
+            const int cx = min(max(__double2int_rd(tc[0]), -2), g.nx + 1);   // = cell_coord
+            const int cy = min(max(__double2int_rd(tc[1]), -2), g.ny + 1);
+            const int cz = min(max(__double2int_rd(tc[2]), -2), g.nz + 1);
+            bool live = true;
+            if (a.nbr_bits) {
+                if (!g.hashed) {
+                    live = false;
+                    if (cx >= -1 && cx <= g.nx && cy >= -1 && cy <= g.ny && cz >= -1 && cz <= g.nz) {
+                        const int kc = (min(max(cz, 0), g.nz - 1) * g.ny + min(max(cy, 0), g.ny - 1)) * g.nx +
+                                       min(max(cx, 0), g.nx - 1);
+                        live = (__ldg(&a.nbr_bits[kc >> 5]) >> (kc & 31)) & 1u;
+                    }
+                } else {
+                    live = stencil_live(a, g, cx, cy, cz);
+                }
+            }
+            if (!live) {
+                // empty 27-cell stencil: every target is beyond its outer faces, at
+                // >= h + (the smallest gap to the own cell's faces); 2h + that gap
+                // if the 5^3-cell neighbourhood is empty too (dense grid)
+                const int cc[3] = {cx, cy, cz};
+                float reach = __fadd_rd(Lout, min_face_gap_t(g, tc, cc));
+                if (a.nbr2_bits && cx >= 0 && cx < g.nx && cy >= 0 && cy < g.ny && cz >= 0 && cz < g.nz) {
+                    const int kc = (cz * g.ny + cy) * g.nx + cx;
+                    if (!((__ldg(&a.nbr2_bits[kc >> 5]) >> (kc & 31)) & 1u)) reach = __fadd_rd(reach, Lout);
+                }
+                a.cert[2 * (size_t)i] = make_float4(__int_as_float(-1),
+                                                    __uint_as_float(cert_pack(pass, __fsub_rd(reach, dmax_hi), a.inv_h_rd)),
+                                                    0.f, 0.f);
+                if (WRITE_CORR) a.corr_out[__float_as_int(p.w)] = -1;
+            }
+            need = live;
+        }
+        a.need[i] = need ? 1 : 0;
+        certified = cv;
+    }
+    accumulate_records(a, vw, lane, cwin, tx, ty, tz, cq, cn, cd2, acc0, acc1);
+    return certified ? 1 : 0;
+}
+
+// TMA rings of the sweep: each warp owns kSweepStages stages of one batch (32
+// consecutive queries: source records + certificates, 1.5 KB), filled by its
+// lane 0 with two 1-D bulk copies (cp.async.bulk) that complete on the stage's
+// mbarrier. The warp consumes batch k while batches k+1..k+3 land; no
+// block-level barrier (warps proceed at their own pace).
+constexpr int kSweepStages = 4;
+struct __align__(128) SweepStage {
+    float4 src[32];
+    float4 cert[64];
+};
+constexpr size_t kSweepSmem = (size_t)(kSweepThreads / 32) * kSweepStages * sizeof(SweepStage);
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void sweep_issue(const K3Args& a, SweepStage* st, uint64_t* bar, int batch) {
+    const int q0 = batch * 32;
+    const int cnt = min(32, a.n - q0);
+    const uint32_t bs = (uint32_t)cnt * 16u, bc = (uint32_t)cnt * 32u;
+    const uint32_t b = smem_u32(bar);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bs + bc) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(smem_u32(st->src)), "l"(a.src + q0), "r"(bs), "r"(b) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(smem_u32(st->cert)), "l"(a.cert + 2 * (size_t)q0), "r"(bc), "r"(b) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    const uint32_t b = smem_u32(bar);
+    uint32_t ok = 0;
+    do {
+        asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                     : "=r"(ok) : "r"(b), "r"(parity) : "memory");
+    } while (!ok);
+}
+
+template <bool WRITE_CORR>
+__global__ void __launch_bounds__(kSweepThreads, 3) k3_sweep(const K3Args a) {
+    extern __shared__ __align__(128) unsigned char sw_smem[];
+    __shared__ __align__(8) uint64_t bar[kSweepThreads / 32][kSweepStages];
+    __shared__ double sT[12];
+    __shared__ __align__(16) float4 sDT[kCertAges][3];
+    __shared__ float sDC[kCertAges];
+    __shared__ float s_rhog;
+    __shared__ __align__(16) double s_vw[kSweepThreads / 32][9 * kVW];
+    __shared__ int s_ncert[kSweepThreads / 32];
+    if (a.st->done || !a.st->cmode) {   // (plain pass: k3_balanced does it all)
+        if (!a.st->done && threadIdx.x < kTermStride)
+            a.block_partials[((size_t)a.part_off + blockIdx.x) * kTermStride + threadIdx.x] = 0.0;
+        return;
+    }
+    const int pass = a.st->passes;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    SweepStage* stages = (SweepStage*)sw_smem + warp * kSweepStages;
+    uint64_t* wbar = bar[warp];
+    const int nb = (a.n + 31) >> 5;
+    const int nw = gridDim.x * (kSweepThreads / 32);
+    const int gw = blockIdx.x * (kSweepThreads / 32) + warp;
+    if (lane == 0) {
+        for (int k = 0; k < kSweepStages; ++k)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&wbar[k])) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        for (int k = 0; k < kSweepStages; ++k)
+            if (gw + k * nw < nb) sweep_issue(a, &stages[k], &wbar[k], gw + k * nw);
+    }
+    if (threadIdx.x < 12) sT[threadIdx.x] = a.st->T[threadIdx.x];
+    if (threadIdx.x >= 32 && threadIdx.x < 32 + kCertAges) cert_tables(a, pass, threadIdx.x - 31, sDT, sDC, &s_rhog);
+    __syncthreads();
+    const GridDev g = a.g;
+    double* vw = s_vw[warp];
+    double acc0 = 0.0, acc1 = 0.0;
+    int ncert = 0;
+    const float Lout = __fmul_rd(a.h_rd, 1.0f - 1.1920928955078125e-07f);
+    const float dmax_hi = __double2float_ru(a.dmax * (1.0 + 9.094947017729282e-13));
+    for (int k = 0;; ++k) {
+        const int b = gw + k * nw;
+        if (b >= nb) break;
+        const int sidx = k % kSweepStages;
+        mbar_wait(&wbar[sidx], (uint32_t)((k / kSweepStages) & 1));
+        const SweepStage& sg = stages[sidx];
+        const float4 p = sg.src[lane];
+        const float4 ca = sg.cert[2 * lane], cb = sg.cert[2 * lane + 1];
+        __syncwarp();   // the warp is done with this stage: refill it
+        if (lane == 0 && b + kSweepStages * nw < nb) sweep_issue(a, &stages[sidx], &wbar[sidx], b + kSweepStages * nw);
+        ncert += sweep_query<WRITE_CORR>(a, g, sT, sDT, sDC, pass, b * 32 + lane, p, ca, cb, Lout, dmax_hi, vw,
+                                         lane, acc0, acc1);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int o = 16; o; o >>= 1) ncert += __shfl_xor_sync(0xffffffffu, ncert, o);
+    if (lane == 0) s_ncert[warp] = ncert;
+    vw[(lane >> 2) * 8 + 2 * (lane & 3)] = acc0;   // C of this warp
+    vw[(lane >> 2) * 8 + 2 * (lane & 3) + 1] = acc1;
+    __syncthreads();
+    if (threadIdx.x < kTermStride) {
+        double s = 0.0;
+        const int ci = a.p2p ? term_cidx_p2p(threadIdx.x) : (threadIdx.x < kTerms ? term_cidx(threadIdx.x) : -1);
+        if (ci >= 0)
+            for (int w = 0; w < kSweepThreads / 32; ++w) s += s_vw[w][ci];
+        if (threadIdx.x == kStatCertified)
+            for (int w = 0; w < kSweepThreads / 32; ++w) s += (double)s_ncert[w];
+        a.block_partials[((size_t)a.part_off + blockIdx.x) * kTermStride + threadIdx.x] = s;
+    }
+}
+
+static void sweep_attrs() {
+    static bool done = false;
+    if (!done) {
+        cudaFuncSetAttribute(k3_sweep<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSweepSmem);
+        cudaFuncSetAttribute(k3_sweep<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSweepSmem);
+        done = true;
+    }
+}
+
+int k3_sweep_blocks_per_sm() {
+    sweep_attrs();
+    int b = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k3_sweep<false>, kSweepThreads, kSweepSmem);
+    return b;
+}
+
+void launch_k3_sweep(const K3Args& a, int blocks, bool write_corr, cudaStream_t s) {
+    sweep_attrs();
+    if (write_corr) k3_sweep<true><<<blocks, kSweepThreads, kSweepSmem, s>>>(a);
+    else k3_sweep<false><<<blocks, kSweepThreads, kSweepSmem, s>>>(a);
 }
 
 template <bool P, bool W>
@@ -1068,10 +1543,16 @@ __device__ static bool horn_fit(const double* terms, double* E) {
 
 // Thread-0 epilogue of a pass (A8): store the 29 terms; in SOLVE mode apply the
 // criteria (R7, R8) and the Gauss-Newton update (Eq. 2, R5, R6) to the state.
-__device__ __noinline__ void tail_finish(const double* terms, IcpState* st, double* hist_fit, double* hist_rmse,
-                            int mode) {
+__device__ __noinline__ void tail_finish(const double* terms, IcpState* st, const TailHist& hist, int mode) {
     for (int k = 0; k < kTerms; ++k) st->terms[k] = terms[k];
     if (mode & TAIL_STEP) return;
+    const int p0 = st->passes;
+    if (p0 < st->hist_cap) {   // the pass's T (before its update) and its terms
+        if (hist.T)
+            for (int k = 0; k < 16; ++k) hist.T[16 * (size_t)p0 + k] = st->T[k];
+        if (hist.terms)
+            for (int k = 0; k < kTermsStats; ++k) hist.terms[kTermStride * (size_t)p0 + k] = terms[k];
+    }
 
     // A8: criteria (R7, R8) then the Gauss-Newton update (Eq. 2, R5, R6)
     const double cnt = terms[27];
@@ -1079,12 +1560,13 @@ __device__ __noinline__ void tail_finish(const double* terms, IcpState* st, doub
     const double rmse = cnt > 0.0 ? sqrt(terms[28] / cnt) : 0.0;
     const int p = st->passes;
     if (p < st->hist_cap) {
-        hist_fit[p] = fit;
-        hist_rmse[p] = rmse;
+        if (hist.fit) hist.fit[p] = fit;
+        if (hist.rmse) hist.rmse[p] = rmse;
     }
     st->passes = p + 1;
     st->fit = fit;
     st->rmse = rmse;
+    st->cmode = fit > 0.5 ? 1 : 0;   // (next pass: certificates once most queries match)
     int done = 0;
     if (p > 0 && fabs(fit - st->fit_prev) < st->rel_fit && fabs(rmse - st->rmse_prev) < st->rel_rmse) {
         st->converged = 1;
@@ -1141,12 +1623,12 @@ __device__ __noinline__ void tail_finish(const double* terms, IcpState* st, doub
 
 __global__ void __launch_bounds__(kTailThreads)
     k_tail(const double* __restrict__ partials, int nblocks, double* gathered, int world, int rank,
-           IcpState* st, double* hist_fit, double* hist_rmse, int mode) {
+           IcpState* st, TailHist hist, int mode) {
     __shared__ double terms[kTermStride];
     if (!(mode & TAIL_STEP) && st->done) return;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (mode & TAIL_REDUCE_BLOCKS) {
-        if (warp < kTerms) {
+        if (warp < kTermsStats) {
             double s = 0.0;
             for (int b = lane; b < nblocks; b += 32) s += partials[(size_t)b * kTermStride + warp];
 #pragma unroll
@@ -1156,12 +1638,12 @@ __global__ void __launch_bounds__(kTailThreads)
         __syncthreads();
         if (mode & TAIL_WRITE_RANK) {
             if (threadIdx.x < kTermStride)
-                gathered[rank * kTermStride + threadIdx.x] = threadIdx.x < kTerms ? terms[threadIdx.x] : 0.0;
+                gathered[rank * kTermStride + threadIdx.x] = threadIdx.x < kTermsStats ? terms[threadIdx.x] : 0.0;
             return;
         }
     }
     if (mode & TAIL_SUM_RANKS) {
-        if (threadIdx.x < kTerms) {
+        if (threadIdx.x < kTermsStats) {
             double s = 0.0;
             for (int r = 0; r < world; ++r) s += gathered[r * kTermStride + threadIdx.x];
             terms[threadIdx.x] = s;
@@ -1169,7 +1651,7 @@ __global__ void __launch_bounds__(kTailThreads)
         __syncthreads();
     }
     if (threadIdx.x != 0) return;
-    tail_finish(terms, st, hist_fit, hist_rmse, mode);
+    tail_finish(terms, st, hist, mode);
 }
 
 // Batched evaluate_registration epilogue: one warp per transform sums the
@@ -1201,9 +1683,8 @@ void launch_eval_reduce(const double* partials, int nblocks, int k, double n_tot
 }
 
 void launch_tail(const double* partials, int nblocks, double* gathered, int world, int rank,
-                 IcpState* st, double* hist_fit, double* hist_rmse, int mode, cudaStream_t s) {
-    k_tail<<<1, kTailThreads, 0, s>>>(partials, nblocks, gathered, world, rank, st, hist_fit,
-                                      hist_rmse, mode);
+                 IcpState* st, TailHist hist, int mode, cudaStream_t s) {
+    k_tail<<<1, kTailThreads, 0, s>>>(partials, nblocks, gathered, world, rank, st, hist, mode);
 }
 
 }  // namespace o3g

@@ -1,4 +1,4 @@
-// k3_sorted.cu — K3 variant 3 (default): the correspondence + reduction pass
+// k3_sorted.cu — K3 variant 3 (O3G_OPT_SEARCH=3; measured slower than the default variant 1): the correspondence + reduction pass
 // organised around a per-block tile of 128 spatially consecutive queries.
 //
 // Same contract and bit-identical correspondences as k3_corr_reduce

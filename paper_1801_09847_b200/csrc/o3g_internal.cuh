@@ -9,6 +9,10 @@ namespace o3g {
 
 constexpr int kTerms = 29;        // O3G_NTERMS
 constexpr int kTermStride = 32;   // padded per-block / per-rank partial
+// per-pass statistics ride in the padding (variant 1; others leave them 0):
+// [29] queries that ran the full search, [30] candidates they scanned, [31]
+// queries settled by a valid certificate (k3_sweep)
+constexpr int kStatSearched = 29, kStatCandidates = 30, kStatCertified = 31, kTermsStats = 32;
 constexpr int kK3Threads = 256;   // correspondence kernel block size
 constexpr int kTailThreads = 1024;
 
@@ -38,7 +42,9 @@ struct IcpState {
     double fit, rmse, fit_prev, rmse_prev;
     double rel_fit, rel_rmse;
     double n_total;
-    int32_t it, max_it, passes, done, flags, converged, hist_cap, pad;
+    int32_t it, max_it, passes, done, flags, converged, hist_cap;
+    int32_t cmode;   // certificates: this pass runs the sweep + certified search (set by
+                     // the previous pass's tail: fitness > 1/2, the refinement phase)
 };
 
 enum TailMode : int {
@@ -155,8 +161,28 @@ struct K3Args {
     const int32_t* tiles;      // variant 4: tile starts in the local source (ntiles)
     int32_t ntiles;
     int ilv;                   // variant 1: 0, or interleaved batches (= ceil(n / 32))
-    int32_t* prev_j;           // variant 1 run loop: per local query, the previous pass's
-                               // winner (sorted target position, -1 none); nullable
+    int32_t* prev_j;           // variant 1 run loop without certificates: per local query,
+                               // the previous pass's winner (sorted target position, -1
+                               // none); nullable
+    // correspondence certificates (variant 1 run loop): per local
+    // query i a 32-byte record cert[2i] = {bits(winner j (sorted position) or -1),
+    // bits((cert pass << 16) | half(rho / h)), q.x, q.y}, cert[2i+1] = {q.z, n.x,
+    // n.y, n.z} (the winner's position and normal, cached: a certified query
+    // streams 32 B and gathers nothing). The result of pass b stays exact at a
+    // later pass while the query has moved by less than rho since pass b.
+    // nullable (= off). With certificates a pass is two kernels: k3_sweep
+    // settles every certified (or bitmap-dead) query and flags the rest in
+    // need[i]; k3_balanced then searches only the flagged ones.
+    float4* cert;
+    uint8_t* need;             // k3_sweep -> k3_balanced: 1 = run the full search
+    int part_off;              // this kernel's first block-partial slot
+    int part_total;            // fused tail: block partials to reduce (all kernels of the pass)
+    double rhog_mul, rhog_cap; // certificate goal: min(mul x last pass's displacement bound, cap x h)
+    const uint32_t* nbr2_bits; // dense grid: the occupancy bitmap dilated twice (bit k set
+                               // iff some cell within Chebyshev distance 2 is occupied)
+    const double* hist_Tr;     // [pass][16]: the T each pass ran with (certificate ages)
+    float smax[3];             // max |source coordinate| per axis (displacement bound)
+    float h_rd, inv_h_rd;      // cell edge h and 1/h, rounded down (rho packing)
     int xsorted;               // target x-sorted inside cells: x-windows in the cooperative path
     int prune;                 // variant 1: row-pruning instantiation (dense grid)
     int prune_min;             //   ... for light queries with >= prune_min candidates
@@ -167,10 +193,14 @@ struct K3Args {
     IcpState* st_rw;
     double* hist_fit;
     double* hist_rmse;
+    double* hist_T;            // per pass: T used and the 29 terms (nullable)
+    double* hist_terms;
 };
+constexpr int kCertAges = 32;     // certificates older than this many passes expire
 // variant: 0 = exact fp64 scan (k3_corr_reduce), 1 = two-pass warp kernel
-// (k3_balanced), 2 = single-pass prefilter (k3_corr_reduce<true>), 3 = tile-sorted
-// two-pass kernel (k3_sorted, default). Identical correspondences.
+// (k3_balanced, the default), 2 = single-pass prefilter (k3_corr_reduce<true>),
+// 3 = tile-sorted two-pass kernel (k3_sorted), 4 = smem-staged tiles (k3_tiled).
+// Identical correspondences.
 constexpr int kTileQ = 128;       // variant 4: queries per tile (max)
 inline int k3_threads(int variant) { return variant == 3 ? 128 : variant == 4 ? kTileQ : kK3Threads; }
 int k3_tiled_blocks_per_sm(bool write_corr);
@@ -178,10 +208,18 @@ void launch_k3_tiled(const K3Args& a, int blocks, bool write_corr, cudaStream_t 
 int k3_sorted_blocks_per_sm(bool write_corr, int hashed);
 void launch_k3_sorted(const K3Args& a, int blocks, bool write_corr, cudaStream_t s);
 void launch_k3(const K3Args& a, int blocks, int variant, bool write_corr, cudaStream_t s);
+int k3_sweep_blocks_per_sm();
+void launch_k3_sweep(const K3Args& a, int blocks, bool write_corr, cudaStream_t s);
 int k3_max_blocks_per_sm(int variant, bool write_corr, int hashed, bool prune);
 void launch_eval_reduce(const double* partials, int nblocks, int k, double n_total, double* fit,
                         double* rmse, cudaStream_t s);
+struct TailHist {
+    double* fit;     // [pass]
+    double* rmse;    // [pass]
+    double* T;       // [pass][16], the T of the pass (before its update)
+    double* terms;   // [pass][kTermStride]
+};
 void launch_tail(const double* block_partials, int nblocks, double* gathered, int world, int rank,
-                 IcpState* st, double* hist_fit, double* hist_rmse, int mode, cudaStream_t s);
+                 IcpState* st, TailHist hist, int mode, cudaStream_t s);
 
 }  // namespace o3g

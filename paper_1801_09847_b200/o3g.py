@@ -27,7 +27,8 @@ FLAG_NO_CORRESPONDENCES = 1
 FLAG_DEGENERATE = 2
 NTERMS = 29
 (OPT_SEARCH, OPT_GRID, OPT_TIMING, OPT_BLOCKS_PER_SM, OPT_NBR_MASK, OPT_COOP_MIN, OPT_ESTIMATION,
- OPT_SOURCE_ORDER, OPT_TARGET_SORT, OPT_PRUNE_MIN, OPT_INTERLEAVE, OPT_XSORT) = range(1, 13)
+ OPT_SOURCE_ORDER, OPT_TARGET_SORT, OPT_PRUNE_MIN, OPT_INTERLEAVE, OPT_XSORT, OPT_CERT,
+ OPT_TRACE_PASS) = range(1, 15)
 
 
 class O3GError(RuntimeError):
@@ -71,6 +72,7 @@ def lib() -> C.CDLL:
             "o3g_dist_init": [P, C.c_int, C.c_int, P],
             "o3g_set_option": [P, C.c_int, I64],
             "o3g_last_run_kernel_ms": [P, P, P, P],
+            "o3g_last_run_trace": [P, P, P, P, P],
             "o3g_grid_info": [P, P, P, P, P],
             "o3g_voxel_down_sample": [P, P, P, I64, D, P, P, P],
             "o3g_evaluate_registration": [P, P, I32, P, P],
@@ -332,7 +334,9 @@ class Context:
         keep: list = []
         ps, n = _pts(source, "source", keep)
         pt, m = _pts(target, "target", keep)
-        pn, _ = _pts(target_normals, "target_normals", keep)
+        pn, mn = _pts(target_normals, "target_normals", keep)
+        if pn is None or mn != m:
+            raise InvalidArgument(ERR_INVALID_ARGUMENT, "target_normals must match target")
         ns = len(voxels)
         vx = np.ascontiguousarray(voxels, np.float64)
         dm = np.ascontiguousarray(dmaxs, np.float64)
@@ -347,6 +351,25 @@ class Context:
                                         fit.ctypes.data, rmse.ctypes.data, its.ctypes.data,
                                         nss.ctypes.data))
         return dict(T=T.reshape(4, 4), fitness=fit, inlier_rmse=rmse, iterations=its, n_source=nss)
+
+    def last_run_trace(self, passes: int, corr_out=None):
+        """o3g_last_run_trace: dict(T [passes,4,4], terms [passes,29], searched
+        [passes], candidates [passes], certified [passes]) of the last run; corr_out (torch CUDA
+        int32 [n_source], optional) gets the correspondences of pass
+        OPT_TRACE_PASS."""
+        T = np.zeros((max(passes, 1), 16))
+        terms = np.zeros((max(passes, 1), NTERMS))
+        stats = np.zeros((max(passes, 1), 3))
+        pc = None
+        if corr_out is not None:
+            import torch
+            if not (_is_torch(corr_out) and corr_out.is_cuda and corr_out.dtype == torch.int32
+                    and corr_out.is_contiguous() and corr_out.numel() == self.n_source):
+                raise InvalidArgument(ERR_INVALID_ARGUMENT, "corr_out must be a contiguous CUDA int32 [n_source] tensor")
+            pc = corr_out.data_ptr()
+        _check(lib().o3g_last_run_trace(self._h, T.ctypes.data, terms.ctypes.data, pc, stats.ctypes.data))
+        return dict(T=T[:passes].reshape(-1, 4, 4), terms=terms[:passes], searched=stats[:passes, 0],
+                    candidates=stats[:passes, 1], certified=stats[:passes, 2])
 
     def last_run_kernel_ms(self):
         k3, n, tail = C.c_double(), C.c_int32(), C.c_double()

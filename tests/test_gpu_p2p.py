@@ -123,10 +123,15 @@ def test_evaluate_perfect_alignment(o3g, workloads):
 # ------------------------------------------------ NEXT(4): normal estimation
 @pytest.mark.parametrize("radius,max_nn", [(0.05, 30), (0.1, 30), (0.03, 8)])
 def test_estimate_normals_parity(o3g, workloads, radius, max_nn):
-    """neighbour sets exact (counts), normals equal to the oracle's
-    (same fp64 mean/covariance order; Jacobi implementations differ, so up to
-    1e-6, and up to sign where the largest component is ambiguous); points
-    with an ill-conditioned smallest eigenvector are skipped."""
+    """neighbour sets exact (counts), normals equal to the oracle's.
+    The device solves the 3x3 eigenproblem in closed form (trigonometric
+    eigenvalue + cross products), the oracle by Jacobi sweeps: two independent
+    methods on the same fp64 covariance, so they agree to the problem's
+    conditioning. EVERY point where they differ by more than fp32 rounding
+    must be justified: its angle must lie within 1e-10 lambda_max / gap
+    (gap = lambda_1 - lambda_0 of the covariance, recomputed here by numpy from
+    the oracle's neighbour set), and a sign flip only where the largest
+    component is ambiguous (S:70)."""
     w = workloads("depth")
     p = w["target"]
     ref_n, ref_c, ref_fb = oracle.estimate_normals(p, radius, max_nn)
@@ -134,18 +139,22 @@ def test_estimate_normals_parity(o3g, workloads, radius, max_nn):
         n, c, fb = ctx.estimate_normals(torch.from_numpy(p).cuda(), radius, max_nn)
     n, c = n.cpu().numpy(), c.cpu().numpy()
     assert np.array_equal(c, ref_c) and fb == ref_fb
-    dot = np.abs((n.astype(np.float64) * ref_n).sum(1))
-    bad = np.nonzero(dot < 1 - 1e-6)[0]
-    # remaining disagreements must be ill-conditioned neighbourhoods
+    n64 = n.astype(np.float64)
+    r64 = ref_n.astype(np.float64)
+    # angle between the lines through the two normals, from the cross product
+    # (accurate for small angles, unlike 1 - dot with fp32 unit vectors)
+    ang = np.linalg.norm(np.cross(n64, r64), axis=1) / (np.linalg.norm(n64, axis=1) * np.linalg.norm(r64, axis=1))
+    bad = np.nonzero(ang > 1e-6)[0]
     p64 = p.astype(np.float64)
-    for i in bad[:50]:
+    for i in bad:
         d = p64 - p64[i]
         d2 = (d[:, 0] * d[:, 0] + d[:, 1] * d[:, 1]) + d[:, 2] * d[:, 2]
         ok = np.nonzero(d2 <= radius * radius)[0]
         nb = ok[np.lexsort((ok, d2[ok]))][:max_nn]
         wv = np.linalg.eigvalsh(np.cov(p64[nb].T, bias=True))
-        assert wv[1] - wv[0] < 1e-5 * max(wv[2], 1e-30), (i, wv)
-    assert len(bad) <= 1e-3 * len(p)
-    same_sign = (n.astype(np.float64) * ref_n).sum(1) > 0
+        gap = wv[1] - wv[0]
+        assert ang[i] <= 1e-10 * wv[2] / max(gap, 1e-300), (i, ang[i], wv)
+    same_sign = (n64 * r64).sum(1) > 0
     amb = np.sort(np.abs(ref_n), 1)
-    assert np.all(same_sign | (amb[:, 2] - amb[:, 1] < 1e-5) | (dot < 1 - 1e-6))
+    flip = np.nonzero(~same_sign & (ang <= 1e-6))[0]
+    assert np.all(amb[flip, 2] - amb[flip, 1] < 1e-6), flip[:10]

@@ -189,13 +189,14 @@ def test_hashed_grid_matches_dense(o3g, workloads):
 
 
 # -------------------------------------------------------- configs: loop
+@pytest.mark.parametrize("grid", list(GRID))
 @pytest.mark.parametrize("name", ["tiny", "depth"])
-def test_loop_parity(o3g, workloads, name):
+def test_loop_parity(o3g, workloads, name, grid):
     w = workloads(name)
     ref = oracle.icp(w["source"], w["target"], w["target_normals"], w["dmax"], w["iters"],
                      init_T=w["init_T"])
     for search in SEARCH:
-        with _ctx(o3g, w, search, order_T=w["init_T"]) as ctx:
+        with _ctx(o3g, w, search, grid, order_T=w["init_T"]) as ctx:
             r = ctx.run(w["init_T"], w["iters"], history=True)
         assert np.abs(r.transformation - ref["T"]).max() <= 1e-6, (name, search)
         assert abs(r.fitness - ref["fitness"]) <= 1e-6
@@ -502,8 +503,10 @@ def test_loop_parity_warm_start(o3g, workloads):
     w = workloads("large16m", n=400_000)
     T0 = w["T_true"] @ _perturb(31, 0.004, 0.01)
     ref = oracle.icp(w["source"], w["target"], w["target_normals"], w["dmax"], 6, init_T=T0)
-    for search in ("balanced", "unpruned"):
-        with _ctx(o3g, w, search, order_T=T0) as ctx:
+    for search, grid, cert in (("balanced", "dense", 1), ("unpruned", "dense", 1), ("balanced", "dense", 0),
+                               ("balanced", "hashed", 1), ("balanced", "hashed", 0)):
+        with _ctx(o3g, w, search, grid, order_T=T0) as ctx:
+            ctx.set_option(o3g.OPT_CERT, cert)
             r = ctx.run(T0, 6, history=True)
         assert np.abs(r.transformation - ref["T"]).max() <= 1e-6, search
         assert abs(r.fitness - ref["fitness"]) <= 1e-6 and abs(r.inlier_rmse - ref["inlier_rmse"]) <= 1e-6
@@ -531,3 +534,87 @@ def test_large16m_converged_regime_sampled(o3g, workloads):
     ref = oracle.step(r.transformation, w["source"], w["target"], w["target_normals"], w["dmax"],
                       grid=grid, subset=sub)
     assert np.array_equal(corr[sub], ref["corr"])
+
+
+# ---------------------------------------- run loop: every pass against the oracle
+def _trace_cases(workloads):
+    big = workloads("large16m", n=400_000)
+    return [("tiny", workloads("tiny"), None, 20, None),
+            ("depth", workloads("depth"), None, 30, None),
+            ("large400k", big, big["T_true"] @ _perturb(31, 0.004, 0.01), 6, None),
+            # T_init regime of the bench config (far from converged, most queries dead)
+            ("large400k_init", big, None, 6, None)]
+
+
+@pytest.mark.parametrize("grid", list(GRID))
+@pytest.mark.parametrize("cert", [1, 0])
+def test_run_loop_every_pass(o3g, workloads, grid, cert):
+    """The run loop's own passes — warm-started searches and, with
+    O3G_OPT_CERT, queries settled by a correspondence certificate (DESIGN.md
+    §5.5) — are only reachable inside o3g_icp_run. o3g_last_run_trace gives
+    the T each pass ran with and its 29 terms: every pass's terms must match
+    the oracle's pass at that T (R14; count exact), and at traced passes the
+    correspondences must be bit-identical. With certificates on, fewer
+    queries run the full search than with them off, and the loop's T is
+    bitwise the same either way."""
+    for name, w, T0, iters, _ in _trace_cases(workloads):
+        T0 = w["init_T"] if T0 is None else T0
+        n = len(w["source"])
+        grid_o = oracle.Grid(w["target"], w["dmax"])
+        with _ctx(o3g, w, "balanced", grid, order_T=T0) as ctx:
+            ctx.set_option(o3g.OPT_CERT, cert)
+            r = ctx.run(T0, iters, 0.0, 0.0)
+            tr = ctx.last_run_trace(r.passes)
+            refs = [oracle.step(T, w["source"], w["target"], w["target_normals"], w["dmax"], grid=grid_o)
+                    for T in tr["T"]]
+            for k, ref in enumerate(refs):
+                _terms_ok(tr["terms"][k], ref)
+                assert tr["terms"][k][27] == ref["count"], (name, k)
+            assert np.array_equal(tr["T"][-1], r.transformation) or r.iterations < r.passes - 1
+            for k in sorted({0, 1, 2, r.passes // 2, r.passes - 1}):
+                ctx.set_option(o3g.OPT_TRACE_PASS, k)
+                corr = torch.full((n,), -7, dtype=torch.int32, device="cuda")
+                r2 = ctx.run(T0, iters, 0.0, 0.0)
+                tk = ctx.last_run_trace(r2.passes, corr)
+                assert np.array_equal(tk["T"], tr["T"]), (name, k)             # deterministic
+                got = corr.cpu().numpy()
+                assert np.array_equal(got, refs[k]["corr"]), (name, grid, cert, k, int((got != refs[k]["corr"]).sum()))
+            ctx.set_option(o3g.OPT_TRACE_PASS, -1)
+            # the other setting: same loop, bit for bit (certificates are exact)
+            ctx.set_option(o3g.OPT_CERT, 1 - cert)
+            r3 = ctx.run(T0, iters, 0.0, 0.0)
+            t3 = ctx.last_run_trace(r3.passes)
+        assert r3.passes == r.passes
+        for k in range(r.passes):
+            _terms_ok(t3["terms"][k], refs[k])
+        on, off = (tr, t3) if cert else (t3, tr)
+        assert on["searched"][0] == off["searched"][0]
+        # (a pass runs with certificates once the previous pass matched > 1/2 of
+        # the source; before that, both settings run the same plain pass)
+        if on["certified"].sum() > 0:
+            assert on["searched"][1:].sum() < off["searched"][1:].sum(), name
+        else:
+            assert np.array_equal(on["searched"], off["searched"]), name
+            assert np.all(np.array([t[27] for t in on["terms"]]) <= len(w["source"]) / 2 + 1) or r.passes <= 1
+        assert off["certified"].sum() == 0
+        assert np.all(on["searched"] <= n) and np.all(on["candidates"] >= 0)
+        assert np.all(on["certified"] + on["searched"] <= n)
+
+
+def test_run_loop_state_reset_between_runs(o3g, workloads):
+    """The run loop's per-query state (certificates / warm-start winners) is
+    reset at the head of every run: a run after a different run on the same
+    context equals the same run on a fresh context, bit for bit."""
+    w = workloads("large16m", n=400_000)
+    Ta = w["T_true"] @ _perturb(51, 0.004, 0.01)
+    Tb = w["T_true"] @ _perturb(52, 0.006, 0.02)
+    for cert in (1, 0):
+        with _ctx(o3g, w, "balanced", order_T=Ta) as ctx:
+            ctx.set_option(o3g.OPT_CERT, cert)
+            ctx.run(Ta, 8, 0.0, 0.0)
+            rb = ctx.run(Tb, 8, 0.0, 0.0)
+        with _ctx(o3g, w, "balanced", order_T=Ta) as ctx:
+            ctx.set_option(o3g.OPT_CERT, cert)
+            fresh = ctx.run(Tb, 8, 0.0, 0.0)
+        assert np.array_equal(rb.transformation, fresh.transformation), cert
+        assert rb.fitness == fresh.fitness and rb.inlier_rmse == fresh.inlier_rmse

@@ -51,6 +51,16 @@ def test_hand_step_golden():
         assert np.array_equal(_upper(r["JTJ"]), np.array(c["jtj_upper"], float)), c["name"]
         assert np.array_equal(r["JTr"], np.array(c["jtr"], float)), c["name"]
         assert r["count"] == c["count"] and r["sum_sq_dist"] == c["sum_sq_dist"], c["name"]
+        # the sums of |term| that scale every R14 tolerance (hand values; the
+        # cancelling case fails an implementation that takes |sum| instead)
+        ab = r["abs_terms"]
+        assert np.array_equal(ab[:21], np.array(c["abs_jtj_upper"], float)), c["name"]
+        assert np.array_equal(ab[21:27], np.array(c["abs_jtr"], float)), c["name"]
+        assert ab[27] == c["count"] and ab[28] == c["sum_sq_dist"], c["name"]
+        # the chunked (OpenMP) pass gives the same terms and sums of |term|
+        rc = oracle.step(np.array(c["T"], float), np.array(c["source"]), np.array(c["target"]),
+                         np.array(c["normals"]), c["dmax"], grid=None, threads=2)
+        assert np.array_equal(rc["terms"], r["terms"]) and np.array_equal(rc["abs_terms"], ab)
         # same answers through the grid accelerator
         rg = oracle.step(np.array(c["T"], float), np.array(c["source"]), np.array(c["target"]),
                          np.array(c["normals"]), c["dmax"], grid=oracle.Grid(np.array(c["target"]), c["dmax"]))
@@ -504,3 +514,47 @@ def test_normals_match_numpy_bruteforce_pca():
     tiny = np.array([[0, 0, 0], [5, 0, 0], [0, 5, 0]], np.float32)
     n, cnt, fb = oracle.estimate_normals(tiny, 0.1, 30)
     assert fb == 3 and np.array_equal(n, np.tile([0, 0, 1], (3, 1)).astype(np.float32))
+
+
+# ------------------------------------------------ deterministic OpenMP mode
+def test_chunked_pass_deterministic_and_equal():
+    """the OpenMP oracle splits the records into fixed chunks and
+    sums the chunk partials in chunk order, so its result is bitwise the same
+    for every thread count; correspondences equal the sequential
+    pass's exactly, the terms within R14 (a different summation order of the
+    same compensated sums), and abs_terms equals an independent numpy sum of
+    |record| over the oracle's own correspondences."""
+    from synth import make
+    w = make("depth")
+    args = (w["init_T"], w["source"], w["target"], w["target_normals"], w["dmax"])
+    seq = oracle.step(*args)
+    outs = [oracle.step(*args, threads=k) for k in (1, 3, 8)]
+    for o in outs:
+        assert np.array_equal(o["corr"], seq["corr"])
+        assert np.array_equal(o["terms"], outs[0]["terms"])
+        assert np.array_equal(o["abs_terms"], outs[0]["abs_terms"])
+    tol = 1e-12 * np.maximum(np.abs(seq["terms"]), seq["abs_terms"])
+    assert np.all(np.abs(outs[0]["terms"] - seq["terms"]) <= tol)
+    # abs_terms from the records, recomputed in numpy (fp64; order-free check)
+    m = seq["corr"] >= 0
+    s = oracle.transform(w["init_T"], w["source"])[m]
+    q = w["target"][seq["corr"][m]].astype(np.float64)
+    n = w["target_normals"][seq["corr"][m]].astype(np.float64)
+    J = np.concatenate([np.cross(s, n), n], 1)
+    r = ((s - q) * n).sum(1)
+    iu = np.triu_indices(6)
+    ab = np.concatenate([np.abs(J[:, iu[0]] * J[:, iu[1]]).sum(0), np.abs(J * r[:, None]).sum(0),
+                         [m.sum(), seq["d2"][m].sum()]])
+    assert np.allclose(seq["abs_terms"], ab, rtol=1e-12, atol=0)
+    assert np.allclose(outs[0]["abs_terms"], ab, rtol=1e-12, atol=0)
+
+
+def test_chunked_icp_matches_sequential():
+    """The OpenMP loop follows the same iterates: same iteration count and
+    flags, T within 1e-9 (the per-pass terms agree within R14)."""
+    from synth import make
+    w = make("tiny")
+    a = oracle.icp(w["source"], w["target"], w["target_normals"], w["dmax"], w["iters"])
+    b = oracle.icp(w["source"], w["target"], w["target_normals"], w["dmax"], w["iters"], threads=4)
+    assert a["iterations"] == b["iterations"] and a["flags"] == b["flags"]
+    assert np.abs(a["T"] - b["T"]).max() <= 1e-9

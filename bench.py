@@ -76,6 +76,15 @@ def oracle_view(w):
     return w["scales"][-1] if "scales" in w else w
 
 
+def l2_peak():
+    """Measured L2 read bandwidth (GB/s) of an L2-resident buffer
+    (tools/microbench/l2_bw.cu, recorded in profiles/l2_bw.json), or None."""
+    p = os.path.join(ROOT, "profiles", "l2_bw.json")
+    if os.path.exists(p):
+        return float(json.load(open(p))["l2_read_gbs"])
+    return None
+
+
 def peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -133,31 +142,64 @@ class Clocks:
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(sm)}
 
 
-def cpu_oracle_rate(w, budget_s=12.0, seed=2024):
-    """Oracle (single thread, as it stands) on a bounded random sample of the
-    source: one correspondence + reduction pass per sampled point at init_T."""
+def host_info():
+    """Core count and CPU model of the box the oracle runs on."""
+    model = None
+    try:
+        for line in subprocess.run(["lscpu"], capture_output=True, text=True).stdout.splitlines():
+            if line.startswith("Model name:"):
+                model = line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return os.cpu_count(), model
+
+
+def cpu_oracle_rate(w, budget_s=8.0, seed=2024, threads=None, brute=False):
+    """Oracle (as it stands) on a bounded random sample of the source: one
+    correspondence + reduction pass per sampled point at init_T.
+    threads None = the sequential pass; k = the deterministic chunked OpenMP
+    pass on k threads; brute = brute-force NN (the
+    definition, 8(d)(iii)) instead of the grid accelerator."""
     import oracle
     from synth.rng import Stream
     t0 = time.perf_counter()
-    grid = oracle.Grid(w["target"], w["dmax"])
+    grid = None if brute else oracle.Grid(w["target"], w["dmax"])
     t_grid = time.perf_counter() - t0
     n = len(w["source"])
-    k = min(n, 2000)
+    k = min(n, 200 if brute else 2000 * (threads or 1))
     idx = Stream(seed).integers(k, n)
     t0 = time.perf_counter()
     oracle.step(w["init_T"], w["source"], w["target"], w["target_normals"], w["dmax"], grid=grid,
-                subset=idx)
+                subset=idx, threads=threads)
     dt = time.perf_counter() - t0
     k2 = int(min(n, max(k, k * budget_s / max(dt, 1e-6))))
     idx = Stream(seed + 1).integers(k2, n)
     t0 = time.perf_counter()
     oracle.step(w["init_T"], w["source"], w["target"], w["target_normals"], w["dmax"], grid=grid,
-                subset=idx)
+                subset=idx, threads=threads)
     dt = time.perf_counter() - t0
-    return dict(value=k2 / dt, unit=UNIT, cores=1, kind="oracle",
+    kind = "oracle-bruteforce" if brute else "oracle"
+    mode = ("brute-force NN" if brute else "grid") + (f", OpenMP {threads} threads (deterministic chunks)"
+                                                     if threads else ", single-threaded")
+    return dict(value=k2 / dt, unit=UNIT, cores=threads or 1, kind=kind,
                 sample=f"{k2} random source points x 1 pass at the start T against the full "
-                       f"{len(w['target'])}-point target (single-threaded C oracle, grid build "
-                       f"{t_grid:.1f}s excluded)")
+                       f"{len(w['target'])}-point target (C oracle, {mode}"
+                       + ("" if brute else f", grid build {t_grid:.1f}s excluded") + ")")
+
+
+def cpu_baselines(w, name):
+    """cpu_baseline: the oracle on 1 thread (the line's value) and on every
+    host core; brute force on the small configs (context)."""
+    import oracle
+    oracle.build()
+    nproc, model = host_info()
+    one = cpu_oracle_rate(w, threads=None)
+    allc = cpu_oracle_rate(w, threads=nproc, seed=2025)
+    out = dict(one, all_cores=allc, nproc=nproc, cpu_model=model,
+               omp_speedup=allc["value"] / one["value"])
+    if name in ("tiny", "depth"):
+        out["brute_force"] = cpu_oracle_rate(w, budget_s=4.0, seed=2026, brute=True)
+    return out
 
 
 def run_reference(a):
@@ -174,7 +216,8 @@ def run_reference(a):
         if s >= a.warmup:
             vals.append(r)
     v = statistics.median([r["value"] for r in vals])
-    cb = dict(vals[-1], value=v)
+    nproc, model = host_info()
+    cb = dict(vals[-1], value=v, nproc=nproc, cpu_model=model)
     out = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": a.gpus,
            "steps": a.steps, "warmup": a.warmup, "ms_per_step": None, "higher_is_better": True,
            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -264,32 +307,34 @@ def main():
     for _ in range(a.warmup):
         units, res = step(src, tgt, nrm)
     barrier()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     l0 = ctx.launch_count()
     # inputs smaller than the 126 MB L2 are flushed (a 256 MB write) before
     # every timed step and only the steps themselves are timed
     in_bytes = 12 * n + 24 * m
     flush = in_bytes < 126 * 2 ** 20
     scratch = torch.empty(256 * 2 ** 20, dtype=torch.uint8, device=dev) if flush else None
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(a.steps)]
+    e_all = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
     with Clocks(local) as clk:
         if not flush:
-            ev0.record()
-            for _ in range(a.steps):
+            e_all[0].record()
+            for k in range(a.steps):
+                ev[k][0].record()
                 units, res = step(src, tgt, nrm)
-            ev1.record()
+                ev[k][1].record()
+            e_all[1].record()
             barrier()
-            ms = ev0.elapsed_time(ev1) / a.steps
+            ms = e_all[0].elapsed_time(e_all[1]) / a.steps
         else:
-            tot = 0.0
-            for _ in range(a.steps):
+            for k in range(a.steps):
                 scratch.fill_(1)
-                ev0.record()
+                ev[k][0].record()
                 units, res = step(src, tgt, nrm)
-                ev1.record()
+                ev[k][1].record()
                 torch.cuda.synchronize()
-                tot += ev0.elapsed_time(ev1)
             barrier()
-            ms = tot / a.steps
+            ms = sum(e0.elapsed_time(e1) for e0, e1 in ev) / a.steps
+    step_ms = [e0.elapsed_time(e1) for e0, e1 in ev]
     launches = (ctx.launch_count() - l0) // a.steps * a.steps
     if world > 1:
         t = torch.tensor([ms], device=dev)
@@ -297,51 +342,91 @@ def main():
         ms = float(t.item())
     value = units / (ms / 1e3)
 
-    # per-pass fitness of one (untimed) registration (SURVEY 8(d) config-5 caveat)
-    hist_fit = None
+    # per-pass detail of one (untimed) registration (SURVEY 8(d) config-5
+    # caveat): fitness, inliers, queries that ran the full search, queries
+    # settled by a certificate, mean candidates per search
+    passes = None
     if not multiscale:
         ctx.set_target(tgt, nrm, w["dmax"])
         ctx.set_source(src, T0)
-        hist_fit = [round(float(f), 6) for f in ctx.run(T0, iters, 0.0, 0.0, history=True).hist_fitness]
+        rh = ctx.run(T0, iters, 0.0, 0.0, history=True)
+        tr = ctx.last_run_trace(rh.passes)
+        passes = [{"fitness": round(float(f), 6), "inliers": int(tr["terms"][k][27]),
+                   "searched": int(tr["searched"][k]), "certified": int(tr["certified"][k]),
+                   "candidates_per_search": round(float(tr["candidates"][k] / max(tr["searched"][k], 1)), 2)}
+                  for k, f in enumerate(rh.hist_fitness)]
 
-    # dominant kernel (K3) live duration with CUDA events inside the run graph
-    ctx.set_option(o3g.o3g.OPT_TIMING, 1)
-    t_loop = []
-    k3 = []
-    for _ in range(3):
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        if multiscale:       # K3 of the finest scale (the last run of the driver)
-            e0.record()
-            units2, r2 = step(src, tgt, nrm)
-            e1.record()
-        else:
-            ctx.set_target(tgt, nrm, w["dmax"])
-            ctx.set_source(src, T0)
-            e0.record()
-            r2 = ctx.run(T0, iters, 0.0, 0.0)
-            e1.record()
-            units2 = n * r2.iterations
-        torch.cuda.synchronize()
-        t_loop.append((e0.elapsed_time(e1), units2))
-        k3_ms, k3_n, tail_ms = ctx.last_run_kernel_ms()
-        k3.append((k3_ms, k3_n, tail_ms))
-    ctx.set_option(o3g.o3g.OPT_TIMING, 0)
-    k3_ms, k3_n, tail_ms = min(k3)
-    k3_avg = k3_ms / k3_n
     hbm, peak_kind = peaks()
+    l2 = l2_peak()
+    n_local_of = lambda nn: (rank + 1) * nn // world - rank * nn // world
+
+    def k3_measure(T_start, reps=3):
+        """Correspondence kernels of every pass (the pass is k3_balanced, or
+        k3_sweep + k3_balanced with certificates), timed live with CUDA events
+        recorded inside the run graph on the stream the kernels run on."""
+        ctx.set_option(o3g.OPT_TIMING, 1)
+        out = []
+        for _ in range(reps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            if multiscale:       # K3 of the finest scale (the last run of the driver)
+                e0.record()
+                units2, r2 = step(src, tgt, nrm)
+                e1.record()
+            else:
+                ctx.set_target(tgt, nrm, w["dmax"])
+                ctx.set_source(src, T_start)
+                e0.record()
+                r2 = ctx.run(T_start, iters, 0.0, 0.0)
+                e1.record()
+                units2 = n * r2.iterations
+            torch.cuda.synchronize()
+            k3_ms, k3_n, tail_ms = ctx.last_run_kernel_ms()
+            out.append((k3_ms, k3_n, tail_ms, e0.elapsed_time(e1), units2, r2))
+        ctx.set_option(o3g.OPT_TIMING, 0)
+        return min(out, key=lambda x: x[0])
+
+    k3_ms, k3_n, tail_ms, loop_ms, loop_units, r2 = k3_measure(T0)
+    k3_avg = k3_ms / k3_n
     if multiscale:
         n_k3 = int(r2["n_source"][-1])
         m_k3 = len(w["scales"][-1]["target"])
     else:
         n_k3, m_k3 = n, m
-    n_local = (rank + 1) * n_k3 // world - rank * n_k3 // world
-    alg_bytes = 12 * n_local + 24 * m_k3 / world
+    alg_bytes = 12 * n_local_of(n_k3) + 24 * m_k3 / world
     achieved = alg_bytes / (k3_avg / 1e3) / 1e9
-    traffic = None
+    traffic_tab = {}
     tp = os.path.join(ROOT, "profiles", "k3_traffic.json")
     if os.path.exists(tp):
-        traffic = json.load(open(tp)).get(f"{a.config}@{world}")
-    loop_ms, loop_units = min(t_loop)
+        traffic_tab = json.load(open(tp))
+    traffic = traffic_tab.get(f"{a.config}@{world}@{a.regime}")
+    # the bound: HBM when the working set exceeds the L2, else the L2 (the
+    # small configs are L2-resident: their HBM fraction is meaningless)
+    if in_bytes >= 126 * 2 ** 20 or l2 is None:
+        roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                "traffic": traffic, "peak_kind": peak_kind}
+    else:
+        roof = {"bound": "l2", "achieved": achieved, "peak": l2, "unit": "GB/s", "frac": achieved / l2,
+                "traffic": traffic, "peak_kind": "measured (tools/microbench/l2_bw.cu, profiles/l2_bw.json)",
+                "hbm_frac": achieved / hbm}
+    roof.update(kernel="correspondence pass: k3_balanced, or k3_sweep + k3_balanced (certificates)",
+                kernel_ms=k3_avg, alg_bytes_per_launch=alg_bytes)
+
+    # the converged regime next to the init one (SURVEY 8(d) caveat; the
+    # default bench starts at the config's init T, where most queries of the
+    # 16M config have no target in reach)
+    converged = None
+    if a.regime == "init" and not multiscale and "T_true" in w:
+        from synth.rng import Stream
+        from synth.scenes import rigid, rotation
+        rs = Stream(0x5EED)
+        Tc = w["T_true"] @ rigid(rotation(rs.unit_vectors(1)[0], np.deg2rad(0.1)), 0.01 * rs.unit_vectors(1)[0])
+        c_k3, c_n, _, c_loop, c_units, c_r = k3_measure(Tc, reps=2)
+        c_ach = alg_bytes / (c_k3 / c_n / 1e3) / 1e9
+        converged = {"init": "T* perturbed by 0.1 deg / 1 cm", "fitness": c_r.fitness,
+                     "loop_ms": c_loop, "loop_src_pt_it_per_s": c_units / (c_loop / 1e3),
+                     "k3_ms_per_pass": c_k3 / c_n, "achieved_gbs": c_ach,
+                     "frac": c_ach / (hbm if roof["bound"] == "hbm" else l2), "bound": roof["bound"],
+                     "traffic": traffic_tab.get(f"{a.config}@{world}@converged")}
 
     # e2e: same metric through the C ABI one-shot call with pinned HOST buffers
     e2e = None
@@ -374,9 +459,7 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
-        import oracle
-        oracle.build()
-        cpu = cpu_oracle_rate(oracle_view(w))
+        cpu = cpu_baselines(oracle_view(w), a.config)
 
     if rank == 0:
         out = {
@@ -392,21 +475,21 @@ def main():
                        "l2": (f"inputs {in_bytes / 1e6:.0f} MB < 126 MB L2: 256 MB write flushes L2 before "
                               "each timed step" if flush else
                               f"inputs {in_bytes / 1e6:.0f} MB > 126 MB L2 (no flush needed)")},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                         "frac": achieved / hbm, "traffic": traffic, "peak_kind": peak_kind,
-                         "kernel": ["k3_corr_reduce<exact>", "k3_balanced", "k3_corr_reduce<prefilter>",
-                                    "k3_sorted", "k3_tiled"][a.search], "kernel_ms": k3_avg,
-                         "alg_bytes_per_launch": alg_bytes},
+            "roofline": roof,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,
             "clocks": clk.summary(),
-            "detail": {"loop_ms": loop_ms, "loop_src_pt_it_per_s": loop_units / (loop_ms / 1e3),
+            "detail": {"step_ms": {"median": statistics.median(step_ms), "min": min(step_ms), "max": max(step_ms),
+                                   "n": len(step_ms)},
+                       "loop_ms": loop_ms, "loop_src_pt_it_per_s": loop_units / (loop_ms / 1e3),
+                       "setup_ms": statistics.median(step_ms) - loop_ms if not multiscale else None,
                        "k3_total_ms": k3_ms, "tail_total_ms": tail_ms, "k3_launches": k3_n,
                        "fitness": (float(res["fitness"][-1]) if multiscale else res.fitness),
                        "inlier_rmse": (float(res["inlier_rmse"][-1]) if multiscale else res.inlier_rmse),
                        "grid": ctx.grid_info(),
-                       "hist_fitness": hist_fit},
+                       "passes": passes,
+                       "converged_regime": converged},
         }
         print(json.dumps(out), flush=True)
     ctx.close()

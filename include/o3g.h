@@ -215,6 +215,24 @@ o3g_status o3g_icp_multiscale(o3g_ctx* ctx, const float* source_xyz, int64_t n_s
 o3g_status o3g_nccl_unique_id(void* id_out_128);
 o3g_status o3g_dist_init(o3g_ctx* ctx, int rank, int world, const void* nccl_unique_id_128);
 
+/* In-process loopback of the multi-GPU path (verification of SURVEY §8(e)
+ * A7 on one device): o3g_dist_init_loopback makes ctx rank `rank` of `world`
+ * WITHOUT a communicator (call it before o3g_set_source, which then keeps the
+ * rank's contiguous shard); o3g_loopback_run drives the world contexts
+ * ctxs[0..world) (ctxs[r] of rank r, all on the same device, same target,
+ * source and options) pass by pass in lockstep on ctxs[0]'s stream: every
+ * rank's correspondence kernels on its shard, its TAIL_WRITE_RANK tail, the
+ * exchange of the world x 29 partial terms (device copies in place of the
+ * NCCL all-gather), and every rank's TAIL_SUM_RANKS tail (rank-order sum +
+ * the A8 update) — the kernels of the distributed path, only the transport
+ * differs. Outputs as o3g_icp_run, from rank 0; O3G_ERR_CUDA if the ranks'
+ * transforms ever differ (they must be bit-identical). o3g_last_run_trace
+ * works on each context afterwards.                                      */
+o3g_status o3g_dist_init_loopback(o3g_ctx* ctx, int rank, int world);
+o3g_status o3g_loopback_run(o3g_ctx* const* ctxs, int world, const double init_T[16],
+                            int32_t max_iterations, double relative_fitness, double relative_rmse,
+                            double T_out[16], double* fitness, double* inlier_rmse, o3g_icp_info* info);
+
 /* -------------------------------------------------------------- options
  * O3G_OPT_SEARCH: correspondence-kernel variant, all bit-identical
  *   (DESIGN.md §5): 0 = exact fp64 test of every candidate; 1 = two-pass

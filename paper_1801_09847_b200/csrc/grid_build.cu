@@ -355,4 +355,16 @@ void launch_fill_i32(int32_t* p, int64_t n, int32_t v, cudaStream_t s) {
     k_fill_i32<<<blocks_for(n, 256), 256, 0, s>>>(p, n, v);
 }
 
+// every 32-byte certificate record's first half := {-1, all ones, 0, 0}
+// (no winner, invalid certificate); the second half is left as it is
+__global__ void k_cert_reset(float4* cert, int64_t n) {
+    const float4 v = make_float4(__int_as_float(-1), __int_as_float(-1), 0.f, 0.f);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        cert[2 * i] = v;
+}
+void launch_cert_reset(float4* cert, int64_t n, cudaStream_t s) {
+    k_cert_reset<<<blocks_for(n, 256), 256, 0, s>>>(cert, n);
+}
+
 }  // namespace o3g

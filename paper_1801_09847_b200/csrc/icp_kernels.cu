@@ -404,24 +404,30 @@ __device__ __forceinline__ bool stencil_live(const K3Args& a, const GridDev& g, 
     return (__ldg(&a.nbr_bits[k >> 5]) >> (k & 31)) & 1u;
 }
 
-template <bool WRITE_CORR, bool COOP, bool PRUNE>
+// CERT: the certificate-mode search of a run with certificates (after
+// k3_sweep: the flagged queries only; rows staged up to the certificate goal;
+// every search leaves a certificate). A run with certificates launches both
+// instantiations every pass; the one that does not match the pass's mode
+// (IcpState::cmode, set on the device by the previous pass) exits at once.
+template <bool WRITE_CORR, bool COOP, bool PRUNE, bool CERT>
 __global__ void __launch_bounds__(kK3Threads, 4) k3_balanced(const K3Args a) {
     extern __shared__ __align__(16) unsigned char k3smem[];
     __shared__ double sT[12];
-    __shared__ __align__(16) float4 sDT[kCertAges][3];   // (certificates: cert_tables)
-    __shared__ float sDC[kCertAges];
+    __shared__ __align__(16) float4 sDT[CERT ? kCertAges : 1][3];   // (certificates: cert_tables)
+    __shared__ float sDC[CERT ? kCertAges : 1];
     __shared__ float s_rhog;
     if (!a.eval_T && a.st->done) return;
-    // certificates: a.cert set (the run loop) and this pass in certificate mode
+    if (a.cert && !a.eval_T && ((a.st->cmode != 0) != CERT || a.st->passes != a.pass_expect))
+        return;   // (the other search instantiation runs this pass)
     // (the warm-start seed is prev_j in both modes)
-    const bool certm = a.cert != nullptr && !a.eval_T && a.st->cmode;
-    const uint8_t* need = certm ? a.need : nullptr;
-    const int pass = certm ? a.st->passes : 0;
+    constexpr bool certm = CERT;
+    const uint8_t* need = CERT ? a.need : nullptr;
+    const int pass = CERT ? a.st->passes : 0;
     if (threadIdx.x < 12) sT[threadIdx.x] = a.eval_T ? a.eval_T[16 * blockIdx.y + threadIdx.x] : a.st->T[threadIdx.x];
-    if (certm && threadIdx.x >= 32 && threadIdx.x < 32 + kCertAges)
+    if (CERT && threadIdx.x >= 32 && threadIdx.x < 32 + kCertAges)
         cert_tables(a, pass, threadIdx.x - 31, sDT, sDC, &s_rhog);
     __syncthreads();
-    const float rhog = certm ? s_rhog : 0.f;
+    const float rhog = CERT ? s_rhog : 0.f;
 
     const GridDev g = a.g;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -618,16 +624,28 @@ __global__ void __launch_bounds__(kK3Threads, 4) k3_balanced(const K3Args a) {
                             face_gaps(sz, g.oz, g.h, cz, gzm, gzp);
                         }
                     }
+                    if (CERT) {
 #pragma unroll
-                    for (int r = 0; r < 9; ++r) {
-                        if (ee[r] > bb[r]) {
-                            const float Lr = row_lower(r % 3 - 1, r / 3 - 1, gym, gyp, gzm, gzp);
-                            if (r == 4 || !(Lr > ub)) {
+                        for (int r = 0; r < 9; ++r) {
+                            if (ee[r] > bb[r]) {
+                                const float Lr = row_lower(r % 3 - 1, r / 3 - 1, gym, gyp, gzm, gzp);
+                                if (r == 4 || !(Lr > ub)) {
+                                    segs[nseg * 32 + lane] = make_int2(bb[r], ee[r]);
+                                    ++nseg;
+                                    c += ee[r] - bb[r];
+                                } else {
+                                    Lskip = fminf(Lskip, Lr);
+                                }
+                            }
+                        }
+                    } else {
+#pragma unroll
+                        for (int r = 0; r < 9; ++r) {
+                            if (ee[r] > bb[r] &&
+                                (r == 4 || !(row_lower(r % 3 - 1, r / 3 - 1, gym, gyp, gzm, gzp) > ub))) {
                                 segs[nseg * 32 + lane] = make_int2(bb[r], ee[r]);
                                 ++nseg;
                                 c += ee[r] - bb[r];
-                            } else {
-                                Lskip = fminf(Lskip, Lr);
                             }
                         }
                     }
@@ -707,11 +725,11 @@ __global__ void __launch_bounds__(kK3Threads, 4) k3_balanced(const K3Args a) {
                                 const int rb = rb0 + (r / 3) * nxny + (r % 3) * g.nx;
                                 if (__fadd_rd(Lr, gxm2) > ub) {
                                     b = __ldg(cs + rb + 1);
-                                    if (b > bb[r]) Lskip = fminf(Lskip, __fadd_rd(Lr, gxm2));
+                                    if (CERT && b > bb[r]) Lskip = fminf(Lskip, __fadd_rd(Lr, gxm2));
                                 }
                                 if (__fadd_rd(Lr, gxp2) > ub) {
                                     e = __ldg(cs + rb + 2);
-                                    if (e < ee[r]) Lskip = fminf(Lskip, __fadd_rd(Lr, gxp2));
+                                    if (CERT && e < ee[r]) Lskip = fminf(Lskip, __fadd_rd(Lr, gxp2));
                                 }
                             }
                             if (e > b) {
@@ -720,7 +738,7 @@ __global__ void __launch_bounds__(kK3Threads, 4) k3_balanced(const K3Args a) {
                                 c += e - b;
                                 rmask |= 1 << t;
                             }
-                        } else {
+                        } else if (CERT) {
                             Lskip = fminf(Lskip, Lr);
                         }
                     }
@@ -749,7 +767,7 @@ __global__ void __launch_bounds__(kK3Threads, 4) k3_balanced(const K3Args a) {
                         if (ub < CUDART_INF_F) {
                             const float Lr = row_lower(y - cy, z - cz, hym, hyp, hzm, hzp);
                             if (Lr > ub) {   // (an empty row also lands here: a valid bound)
-                                Lskip = fminf(Lskip, Lr);
+                                if (CERT) Lskip = fminf(Lskip, Lr);
                                 continue;
                             }
                         }
@@ -976,7 +994,7 @@ __global__ void __launch_bounds__(kK3Threads, 4) k3_balanced(const K3Args a) {
         }
 
         // decision (exact fp64 rule, R1-R3)
-        bool uniq = !heavy;   // (certificates: the decision had a unique nearest candidate)
+        bool uniq = CERT && !heavy;   // (certificates: the decision had a unique nearest candidate)
         if (!heavy && c > 0 && m1 <= thr0) {
             const float4 t = __ldg(&a.tpos[j1]);
             const double dx = __dsub_rn(sx, (double)t.x), dy = __dsub_rn(sy, (double)t.y),
@@ -987,7 +1005,7 @@ __global__ void __launch_bounds__(kK3Threads, 4) k3_balanced(const K3Args a) {
                 if (d2 <= r2) { win = j1, widx = __float_as_int(t.w), wd2 = d2, wq = t; }
             } else {
                 // near-tie (or duplicate visit): exact filtered rescan
-                uniq = false;
+                if (CERT) uniq = false;
                 double bd = CUDART_INF;
                 int bidx = INT_MAX;
                 float thr = thr0;
@@ -1014,7 +1032,7 @@ __global__ void __launch_bounds__(kK3Threads, 4) k3_balanced(const K3Args a) {
         if (WRITE_CORR && i < a.n) a.corr_out[__float_as_int(p.w)] = widx;
         float4 wn = make_float4(0.f, 0.f, 0.f, 0.f);   // the winner's normal (plane records)
         if (win >= 0 && !a.p2p) wn = __ldg(&a.tnrm[win]);
-        if (certm && i < a.n) {
+        if (CERT && i < a.n) {
             // certificate of this search: every target other than the winner is at
             // >= L2 (scanned candidates by their prefilter values, unstaged rows /
             // cells by their bounds, the rest of the grid beyond the stencil's
@@ -1246,7 +1264,7 @@ __global__ void __launch_bounds__(kSweepThreads, 3) k3_sweep(const K3Args a) {
     __shared__ float s_rhog;
     __shared__ __align__(16) double s_vw[kSweepThreads / 32][9 * kVW];
     __shared__ int s_ncert[kSweepThreads / 32];
-    if (a.st->done || !a.st->cmode) {   // (plain pass: k3_balanced does it all)
+    if (a.st->done || !a.st->cmode || a.st->passes != a.pass_expect) {   // (plain pass: k3_balanced does it all)
         if (!a.st->done && threadIdx.x < kTermStride)
             a.block_partials[((size_t)a.part_off + blockIdx.x) * kTermStride + threadIdx.x] = 0.0;
         return;
@@ -1334,16 +1352,16 @@ static int occ_of() {
     return b;
 }
 
-template <bool W, bool CO, bool PR>
+template <bool W, bool CO, bool PR, bool CE>
 static int occ_v2(int hashed) {
     static bool attr_done = false;
     if (!attr_done) {
-        cudaFuncSetAttribute(k3_balanced<W, CO, PR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(k3_balanced<W, CO, PR, CE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)k3v2_smem(1));
         attr_done = true;
     }
     int b = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k3_balanced<W, CO, PR>, kK3Threads, k3v2_smem(hashed));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k3_balanced<W, CO, PR, CE>, kK3Threads, k3v2_smem(hashed));
     return b;
 }
 
@@ -1353,12 +1371,33 @@ int k3_max_blocks_per_sm(int variant, bool write_corr, int hashed, bool prune) {
         case 2: return write_corr ? occ_of<true, true>() : occ_of<true, false>();
         case 3: return k3_sorted_blocks_per_sm(write_corr, hashed);
         case 4: return k3_tiled_blocks_per_sm(write_corr);
-        default:   // the cooperative instantiation has the same footprint class
-            if (prune) return write_corr ? occ_v2<true, false, true>(hashed) : occ_v2<false, false, true>(hashed);
-            return write_corr ? occ_v2<true, false, false>(hashed) : occ_v2<false, false, false>(hashed);
+        default:   // the cooperative / certificate instantiations have the same footprint class
+            if (prune) return write_corr ? occ_v2<true, false, true, false>(hashed) : occ_v2<false, false, true, false>(hashed);
+            return write_corr ? occ_v2<true, false, false, false>(hashed) : occ_v2<false, false, false, false>(hashed);
     }
 }
 
+template <bool CE>
+static void launch_balanced(const K3Args& a, int sel, dim3 grid, size_t sm, cudaStream_t s) {
+    occ_v2<true, false, false, CE>(a.g.hashed), occ_v2<false, false, false, CE>(a.g.hashed);
+    occ_v2<true, true, false, CE>(a.g.hashed), occ_v2<false, true, false, CE>(a.g.hashed);
+    occ_v2<true, false, true, CE>(a.g.hashed), occ_v2<false, false, true, CE>(a.g.hashed);
+    occ_v2<true, true, true, CE>(a.g.hashed), occ_v2<false, true, true, CE>(a.g.hashed);
+    switch (sel) {
+        case 0: k3_balanced<false, false, false, CE><<<grid, kK3Threads, sm, s>>>(a); break;
+        case 1: k3_balanced<false, false, true, CE><<<grid, kK3Threads, sm, s>>>(a); break;
+        case 2: k3_balanced<false, true, false, CE><<<grid, kK3Threads, sm, s>>>(a); break;
+        case 3: k3_balanced<false, true, true, CE><<<grid, kK3Threads, sm, s>>>(a); break;
+        case 4: k3_balanced<true, false, false, CE><<<grid, kK3Threads, sm, s>>>(a); break;
+        case 5: k3_balanced<true, false, true, CE><<<grid, kK3Threads, sm, s>>>(a); break;
+        case 6: k3_balanced<true, true, false, CE><<<grid, kK3Threads, sm, s>>>(a); break;
+        default: k3_balanced<true, true, true, CE><<<grid, kK3Threads, sm, s>>>(a); break;
+    }
+}
+
+// variant 1 with certificates (a.cert set): both search instantiations are
+// launched, the plain one first; each exits at once unless its mode is the
+// pass's (so a pass in either mode costs one extra empty launch)
 void launch_k3(const K3Args& a, int blocks, int variant, bool write_corr, cudaStream_t s) {
     switch (variant) {
         case 0:
@@ -1373,22 +1412,10 @@ void launch_k3(const K3Args& a, int blocks, int variant, bool write_corr, cudaSt
         case 4: launch_k3_tiled(a, blocks, write_corr, s); break;
         default: {
             const size_t sm = k3v2_smem(a.g.hashed);
-            occ_v2<true, false, false>(a.g.hashed), occ_v2<false, false, false>(a.g.hashed);
-            occ_v2<true, true, false>(a.g.hashed), occ_v2<false, true, false>(a.g.hashed);
-            occ_v2<true, false, true>(a.g.hashed), occ_v2<false, false, true>(a.g.hashed);
-            occ_v2<true, true, true>(a.g.hashed), occ_v2<false, true, true>(a.g.hashed);
             const dim3 grid(blocks, a.eval_T ? a.n_eval : 1);
             const int sel = (write_corr ? 4 : 0) | (a.coop_min > 0 ? 2 : 0) | (a.prune ? 1 : 0);
-            switch (sel) {
-                case 0: k3_balanced<false, false, false><<<grid, kK3Threads, sm, s>>>(a); break;
-                case 1: k3_balanced<false, false, true><<<grid, kK3Threads, sm, s>>>(a); break;
-                case 2: k3_balanced<false, true, false><<<grid, kK3Threads, sm, s>>>(a); break;
-                case 3: k3_balanced<false, true, true><<<grid, kK3Threads, sm, s>>>(a); break;
-                case 4: k3_balanced<true, false, false><<<grid, kK3Threads, sm, s>>>(a); break;
-                case 5: k3_balanced<true, false, true><<<grid, kK3Threads, sm, s>>>(a); break;
-                case 6: k3_balanced<true, true, false><<<grid, kK3Threads, sm, s>>>(a); break;
-                default: k3_balanced<true, true, true><<<grid, kK3Threads, sm, s>>>(a); break;
-            }
+            launch_balanced<false>(a, sel, grid, sm, s);
+            if (a.cert && !a.eval_T) launch_balanced<true>(a, sel, grid, sm, s);
         }
     }
 }

@@ -182,6 +182,7 @@ struct o3g_ctx {
     int graph_launches = 0;        // our kernels per graph launch
     // distributed
     int rank = 0, world = 1;
+    bool loopback = false;         // o3g_dist_init_loopback: no communicator (o3g_loopback_run)
     nccl_comm_t comm = nullptr;
     // stats
     int64_t launches = 0;
@@ -781,6 +782,7 @@ static K3Args k3_args(o3g_ctx* c, int32_t* corr) {
     a.part_total = 0;
     a.rhog_mul = c->rhog_mul;
     a.rhog_cap = c->rhog_cap;
+    a.pass_expect = -1;
     a.nbr2_bits = (a.nbr_bits && !c->g.hashed) ? c->nbr_c.as<uint32_t>() : nullptr;
     a.hist_Tr = c->hist_T.as<double>();
     for (int k = 0; k < 3; ++k) a.smax[k] = c->smax[k];
@@ -801,18 +803,29 @@ static K3Args k3_args(o3g_ctx* c, int32_t* corr) {
 // queries), then the tail (with the rank exchange when distributed). sblocks:
 // the sweep's grid (0 = no certificates); block partials [0, sblocks) are the
 // sweep's, [sblocks, sblocks + blocks) the search's.
+// phase (world > 1): 0 = the whole pass (NCCL all-gather); 1 = up to this rank's
+// TAIL_WRITE_RANK; 2 = only the TAIL_SUM_RANKS tail (the loopback transport
+// exchanges the slots between the two).
 static o3g_status enqueue_pass(o3g_ctx* c, int blocks, bool write_corr, int32_t* corr,
                                int tail_mode, cudaEvent_t ev0, cudaEvent_t ev1, int* nlaunch,
-                               int32_t* prev_j = nullptr, float4* cert = nullptr, int sblocks = 0) {
+                               int32_t* prev_j = nullptr, float4* cert = nullptr, int sblocks = 0,
+                               int phase = 0, int pass = -1) {
     const TailHist hist{c->hist_fit.as<double>(), c->hist_rmse.as<double>(), c->hist_T.as<double>(),
                         c->hist_terms.as<double>()};
     if (ev0) CK(cudaEventRecordWithFlags(ev0, c->exec, cudaEventRecordExternal));
     const bool fused = c->world == 1 && k3_variant(c) == 1 && c->n_local > 0;
     if (c->estimation) tail_mode |= TAIL_P2P;
+    if (phase == 2) {
+        launch_tail(nullptr, 0, c->gathered.as<double>(), c->world, c->rank, c->state.as<IcpState>(), hist,
+                    TAIL_SUM_RANKS | tail_mode, c->exec);
+        ++*nlaunch;
+        return O3G_OK;
+    }
     if (c->n_local > 0) {
         K3Args ka = k3_args(c, corr);
         ka.prev_j = prev_j;
         ka.cert = cert;
+        ka.pass_expect = pass;
         ka.part_total = blocks;
         if (cert && sblocks > 0) {
             ka.need = c->need.as<uint8_t>();
@@ -831,7 +844,7 @@ static o3g_status enqueue_pass(o3g_ctx* c, int blocks, bool write_corr, int32_t*
             ka.hist_terms = hist.terms;
         }
         launch_k3(ka, blocks, k3_variant(c), write_corr, c->exec);
-        ++*nlaunch;
+        *nlaunch += (ka.cert && k3_variant(c) == 1) ? 2 : 1;   // (both search instantiations)
     }
     if (ev1) CK(cudaEventRecordWithFlags(ev1, c->exec, cudaEventRecordExternal));
     const int nb = c->n_local > 0 ? blocks + (cert ? sblocks : 0) : 0;
@@ -845,6 +858,11 @@ static o3g_status enqueue_pass(o3g_ctx* c, int blocks, bool write_corr, int32_t*
     } else {
         launch_tail(c->partials.as<double>(), nb, gat, c->world, c->rank, st, TailHist{},
                     TAIL_REDUCE_BLOCKS | TAIL_WRITE_RANK | (tail_mode & TAIL_STEP), c->exec);
+        if (phase == 1) {
+            ++*nlaunch;
+            return O3G_OK;
+        }
+        if (!c->comm) return fail(O3G_ERR_COMM, "no communicator (a loopback context runs through o3g_loopback_run)");
         nccl_result_t r = nccl().all_gather(gat + (size_t)c->rank * kTermStride, gat, kTermStride,
                                             kNcclFloat64, c->comm, c->exec);
         if (r != 0) return fail(O3G_ERR_COMM, std::string("ncclAllGather: ") +
@@ -921,6 +939,27 @@ static int sweep_blocks(const o3g_ctx* c) {
     return (int)(b < 1 ? 1 : b);
 }
 
+// Per-run state (enqueued on c->exec): the first pass has no previous winners
+// or certificates, every entry starts at -1 (a certificate of all ones is
+// invalid; only the first 16 bytes of each 32-byte record);
+// the traced correspondences start at -2 (not this rank's).
+static o3g_status run_state_buffers(o3g_ctx* c, bool certm, bool trace) {
+    TRY(c->prevj.ensure((size_t)(c->n_local > 0 ? c->n_local : 1) * 4));
+    if (certm) {
+        TRY(c->cert.ensure((size_t)c->n_local * 2 * sizeof(float4)));
+        TRY(c->need.ensure((size_t)c->n_local + 256));   // (+ a zero tail: flags are read 8 at a time)
+    }
+    if (trace) TRY(c->trace_corr.ensure((size_t)c->n_total * 4));
+    return O3G_OK;
+}
+static o3g_status run_prologue(o3g_ctx* c, bool certm, bool trace) {
+    if (c->n_local > 0) CK(cudaMemsetAsync(c->prevj.p, 0xFF, (size_t)c->n_local * 4, c->exec));
+    if (c->n_local > 0 && certm) launch_cert_reset(c->cert.as<float4>(), c->n_local, c->exec);
+    if (certm) CK(cudaMemsetAsync(c->need.as<uint8_t>() + c->n_local, 0, 256, c->exec));
+    if (trace) launch_fill_i32(c->trace_corr.as<int32_t>(), c->n_total, -2, c->exec);
+    return O3G_OK;
+}
+
 static o3g_status build_graph(o3g_ctx* c, int max_it, int blocks, int sblocks) {
     GraphKey key;
     key.max_it = max_it + 1000000 * c->estimation;
@@ -933,12 +972,7 @@ static o3g_status build_graph(o3g_ctx* c, int max_it, int blocks, int sblocks) {
     const bool trace = c->trace_pass >= 0 && c->trace_pass <= max_it;
     // the run loop's per-query state: the previous winner (warm start) and,
     // with certificates, the 32-byte records and the sweep's search flags
-    TRY(c->prevj.ensure((size_t)(c->n_local > 0 ? c->n_local : 1) * 4));
-    if (certm) {
-        TRY(c->cert.ensure((size_t)c->n_local * 2 * sizeof(float4)));
-        TRY(c->need.ensure((size_t)c->n_local + 256));   // (+ a zero tail: flags are read 8 at a time)
-    }
-    if (trace) TRY(c->trace_corr.ensure((size_t)c->n_total * 4));
+    TRY(run_state_buffers(c, certm, trace));
     const void* ptrs[12] = {c->src4.p, c->tpos.p, c->tnrm.p, c->cell_start.p, c->partials.p,
                             c->state.p, c->hist_fit.p, c->gathered.p, c->hist_T.p, c->hist_terms.p,
                             certm ? c->cert.p : c->prevj.p, trace ? c->trace_corr.p : c->need.p};
@@ -952,14 +986,14 @@ static o3g_status build_graph(o3g_ctx* c, int max_it, int blocks, int sblocks) {
         c->events.push_back(ev);
     }
     CK(cudaStreamBeginCapture(c->exec, cudaStreamCaptureModeThreadLocal));
-    // the first pass has no previous winners / certificates: every entry starts
-    // at -1 (a certificate of all ones is invalid)
-    // (certificates: the first 16 bytes of every 32-byte record, a strided memset)
-    if (c->n_local > 0) CK(cudaMemsetAsync(c->prevj.p, 0xFF, (size_t)c->n_local * 4, c->exec));
-    if (c->n_local > 0 && certm) CK(cudaMemset2DAsync(c->cert.p, 32, 0xFF, 16, (size_t)c->n_local, c->exec));
-    if (certm) CK(cudaMemsetAsync(c->need.as<uint8_t>() + c->n_local, 0, 256, c->exec));
-    if (trace) launch_fill_i32(c->trace_corr.as<int32_t>(), c->n_total, -2, c->exec);
-    int nl = trace ? 1 : 0;
+    o3g_status st0 = run_prologue(c, certm, trace);
+    if (st0 != O3G_OK) {
+        cudaGraph_t g0 = nullptr;
+        cudaStreamEndCapture(c->exec, &g0);
+        if (g0) cudaGraphDestroy(g0);
+        return st0;
+    }
+    int nl = (trace ? 1 : 0) + (certm && c->n_local > 0 ? 1 : 0);
     o3g_status st = O3G_OK;
     for (int p = 0; p <= max_it && st == O3G_OK; ++p) {
         const bool wc = trace && p == c->trace_pass;
@@ -967,7 +1001,7 @@ static o3g_status build_graph(o3g_ctx* c, int max_it, int blocks, int sblocks) {
                           c->timing ? c->events[2 * p] : nullptr,
                           c->timing ? c->events[2 * p + 1] : nullptr, &nl,
                           c->prevj.as<int32_t>(), certm ? c->cert.as<float4>() : nullptr,
-                          certm ? sblocks : 0);
+                          certm ? sblocks : 0, 0, p);
     }
     cudaGraph_t graph = nullptr;
     cudaError_t e = cudaStreamEndCapture(c->exec, &graph);
@@ -1002,6 +1036,7 @@ o3g_status o3g_icp_run(o3g_ctx* c, const double init_T[16], int32_t max_iteratio
     if (!c->src_ready) return fail(O3G_ERR_INVALID_ARGUMENT, "o3g_set_target and o3g_set_source must be called first");
     if (!T_out || !fitness || !inlier_rmse) return fail(O3G_ERR_INVALID_ARGUMENT, "T_out, fitness and inlier_rmse are required");
     if (!c->estimation && !c->has_normals) return fail(O3G_ERR_INVALID_ARGUMENT, "point-to-plane needs target normals");
+    if (c->loopback) return fail(O3G_ERR_INVALID_ARGUMENT, "a loopback context runs through o3g_loopback_run");
     TRY(enter(c));
     const int blocks = k3_blocks(c, false);
     const int sblocks = cert_on(c, max_iterations) ? sweep_blocks(c) : 0;
@@ -1114,6 +1149,7 @@ o3g_status o3g_dist_init(o3g_ctx* c, int rank, int world, const void* id) {
     CK(cudaSetDevice(c->device));
     invalidate_graph(c);
     c->src_ready = false;
+    c->loopback = false;
     if (c->comm && nccl().comm_destroy) nccl().comm_destroy(c->comm);
     c->comm = nullptr;
     c->rank = rank;
@@ -1129,6 +1165,112 @@ o3g_status o3g_dist_init(o3g_ctx* c, int rank, int world, const void* id) {
         c->rank = 0;
         return fail(O3G_ERR_COMM, std::string("ncclCommInitRank: ") +
                                       (nccl().error_string ? nccl().error_string(r) : "?"));
+    }
+    return O3G_OK;
+}
+
+o3g_status o3g_dist_init_loopback(o3g_ctx* c, int rank, int world) {
+    if (!c) return fail(O3G_ERR_INVALID_ARGUMENT, "ctx is NULL");
+    if (world < 1 || rank < 0 || rank >= world) return fail(O3G_ERR_INVALID_ARGUMENT, "bad rank/world");
+    TRY(o3g_dist_init(c, 0, 1, nullptr));
+    c->rank = rank;
+    c->world = world;
+    c->loopback = world > 1;
+    return O3G_OK;
+}
+
+o3g_status o3g_loopback_run(o3g_ctx* const* ctxs, int world, const double init_T[16], int32_t max_iterations,
+                            double relative_fitness, double relative_rmse, double T_out[16], double* fitness,
+                            double* inlier_rmse, o3g_icp_info* info) {
+    if (!ctxs || world < 1 || world > 64) return fail(O3G_ERR_INVALID_ARGUMENT, "need 1 <= world <= 64 contexts");
+    if (!rigid_ok(init_T)) return fail(O3G_ERR_INVALID_ARGUMENT, "init_T is not a rigid transform");
+    if (max_iterations < 0 || max_iterations > 100000) return fail(O3G_ERR_INVALID_ARGUMENT, "max_iterations must be in [0, 100000]");
+    if (!(relative_fitness >= 0.0) || !(relative_rmse >= 0.0)) return fail(O3G_ERR_INVALID_ARGUMENT, "criteria must be >= 0");
+    if (!T_out || !fitness || !inlier_rmse) return fail(O3G_ERR_INVALID_ARGUMENT, "T_out, fitness and inlier_rmse are required");
+    for (int r = 0; r < world; ++r) {
+        o3g_ctx* c = ctxs[r];
+        if (!c || c->rank != r || c->world != world || (world > 1 && !c->loopback))
+            return fail(O3G_ERR_INVALID_ARGUMENT, "ctxs[r] must be loopback rank r of world");
+        if (!c->src_ready) return fail(O3G_ERR_INVALID_ARGUMENT, "o3g_set_target and o3g_set_source must be called first");
+        if (!c->estimation && !c->has_normals) return fail(O3G_ERR_INVALID_ARGUMENT, "point-to-plane needs target normals");
+        if (c->device != ctxs[0]->device) return fail(O3G_ERR_INVALID_ARGUMENT, "loopback contexts share one device");
+    }
+    TRY(enter(ctxs[0]));
+    // every rank's work goes on ctxs[0]'s stream, in lockstep
+    std::vector<cudaStream_t> saved(world);
+    for (int r = 0; r < world; ++r) saved[r] = ctxs[r]->exec, ctxs[r]->exec = ctxs[0]->exec;
+    auto body = [&]() -> o3g_status {
+        std::vector<int> blocks(world), sblocks(world);
+        std::vector<bool> certm(world), trace(world);
+        for (int r = 0; r < world; ++r) {
+            o3g_ctx* c = ctxs[r];
+            invalidate_graph(c);
+            blocks[r] = k3_blocks(c, false);
+            sblocks[r] = cert_on(c, max_iterations) ? sweep_blocks(c) : 0;
+            certm[r] = sblocks[r] > 0;
+            trace[r] = c->trace_pass >= 0 && c->trace_pass <= max_iterations;
+            TRY(loop_buffers(c, blocks[r] + sblocks[r], max_iterations + 1));
+            TRY(run_state_buffers(c, certm[r], trace[r]));
+            init_state(c, init_T, max_iterations, relative_fitness, relative_rmse, max_iterations + 1);
+            CK(cudaMemcpyAsync(c->state.p, c->h_state, sizeof(IcpState), cudaMemcpyHostToDevice, c->exec));
+            CK(cudaStreamSynchronize(c->exec));   // (h_state is reused below)
+            TRY(run_prologue(c, certm[r], trace[r]));
+        }
+        int nl = 0;
+        for (int p = 0; p <= max_iterations; ++p) {
+            for (int r = 0; r < world; ++r) {
+                o3g_ctx* c = ctxs[r];
+                const bool wc = trace[r] && p == c->trace_pass;
+                TRY(enqueue_pass(c, blocks[r], wc, wc ? c->trace_corr.as<int32_t>() : nullptr, TAIL_SOLVE, nullptr,
+                                 nullptr, &nl, c->prevj.as<int32_t>(), certm[r] ? c->cert.as<float4>() : nullptr,
+                                 certm[r] ? sblocks[r] : 0, world > 1 ? 1 : 0, p));
+            }
+            if (world == 1) continue;
+            // the transport: rank r's slot of its gathered buffer -> every other rank's
+            for (int r = 0; r < world; ++r)
+                for (int q = 0; q < world; ++q)
+                    if (q != r)
+                        CK(cudaMemcpyAsync(ctxs[q]->gathered.as<double>() + (size_t)r * kTermStride,
+                                           ctxs[r]->gathered.as<double>() + (size_t)r * kTermStride,
+                                           kTermStride * sizeof(double), cudaMemcpyDeviceToDevice, ctxs[0]->exec));
+            for (int r = 0; r < world; ++r) {
+                o3g_ctx* c = ctxs[r];
+                TRY(enqueue_pass(c, blocks[r], false, nullptr, TAIL_SOLVE, nullptr, nullptr, &nl, nullptr, nullptr,
+                                 0, 2));
+            }
+        }
+        for (int r = 0; r < world; ++r) ctxs[r]->launches += nl / world;
+        return O3G_OK;
+    };
+    o3g_status st = body();
+    for (int r = 0; r < world; ++r) ctxs[r]->exec = saved[r];
+    TRY(st);
+    CK(cudaStreamSynchronize(ctxs[0]->exec));
+    CK(cudaGetLastError());
+    IcpState s0;
+    for (int r = 0; r < world; ++r) {
+        o3g_ctx* c = ctxs[r];
+        IcpState sr;
+        CK(cudaMemcpy(&sr, c->state.p, sizeof(IcpState), cudaMemcpyDeviceToHost));
+        if (r == 0) s0 = sr;
+        else if (memcmp(sr.T, s0.T, sizeof(s0.T)) || sr.passes != s0.passes || sr.flags != s0.flags)
+            return fail(O3G_ERR_CUDA, "loopback ranks diverged");
+        c->last_passes = sr.passes;
+        c->trace_valid = c->trace_pass >= 0 && c->trace_pass < sr.passes;
+        c->last_k3_ms = 0.0;
+        c->last_k3_launches = 0;
+    }
+    memcpy(T_out, s0.T, 16 * sizeof(double));
+    *fitness = s0.fit;
+    *inlier_rmse = s0.rmse;
+    if (info) {
+        info->iterations = s0.it;
+        info->passes = s0.passes;
+        info->converged = s0.converged;
+        info->flags = s0.flags;
+        info->fitness = s0.fit;
+        info->inlier_rmse = s0.rmse;
+        info->inlier_count = s0.terms[27];
     }
     return O3G_OK;
 }

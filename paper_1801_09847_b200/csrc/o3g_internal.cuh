@@ -114,6 +114,7 @@ void launch_gather_target(const float* xyz, const float* nrm, const int32_t* val
 void launch_gather_source(const float* xyz, const int32_t* vals_sorted, int64_t lo, int64_t hi,
                           float4* out, cudaStream_t s);
 void launch_fill_i32(int32_t* p, int64_t n, int32_t v, cudaStream_t s);
+void launch_cert_reset(float4* cert, int64_t n, cudaStream_t s);
 // dilated occupancy bitmap of a dense grid: occupancy from cell_start, then
 // three shifted-OR passes (x by 1, y by nx, z by nx*ny). Bits that wrap across
 // row / slab boundaries only add false positives (a query then just does the
@@ -178,6 +179,9 @@ struct K3Args {
     int part_off;              // this kernel's first block-partial slot
     int part_total;            // fused tail: block partials to reduce (all kernels of the pass)
     double rhog_mul, rhog_cap; // certificate goal: min(mul x last pass's displacement bound, cap x h)
+    int pass_expect;           // run loop: the pass this launch belongs to (-1: no check); a
+                               // kernel finding IcpState::passes != pass_expect exits (the
+                               // pass's other search instantiation already ran its tail)
     const uint32_t* nbr2_bits; // dense grid: the occupancy bitmap dilated twice (bit k set
                                // iff some cell within Chebyshev distance 2 is occupied)
     const double* hist_Tr;     // [pass][16]: the T each pass ran with (certificate ages)

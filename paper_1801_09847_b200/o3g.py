@@ -70,6 +70,8 @@ def lib() -> C.CDLL:
             "o3g_icp_run": [P, P, I32, D, D, P, P, P, P, P, P],
             "o3g_nccl_unique_id": [P],
             "o3g_dist_init": [P, C.c_int, C.c_int, P],
+            "o3g_dist_init_loopback": [P, C.c_int, C.c_int],
+            "o3g_loopback_run": [P, C.c_int, P, I32, D, D, P, P, P, P],
             "o3g_set_option": [P, C.c_int, I64],
             "o3g_last_run_kernel_ms": [P, P, P, P],
             "o3g_last_run_trace": [P, P, P, P, P],
@@ -197,6 +199,20 @@ def icp_point_to_point(source, target, max_correspondence_distance, init=None,
     return _result(T, fit, rmse, info)
 
 
+def loopback_run(ctxs, init=None, max_iterations=30, relative_fitness=1e-6,
+                 relative_rmse=1e-6) -> RegistrationResult:
+    """o3g_loopback_run: the multi-GPU loop of the contexts ctxs (ranks 0..P-1,
+    one device) in lockstep, the all-gather done by device copies."""
+    keep: list = []
+    arr = (C.c_void_p * len(ctxs))(*[c._h.value for c in ctxs])
+    T = np.zeros(16)
+    fit, rmse, info = C.c_double(), C.c_double(), _Info()
+    _check(lib().o3g_loopback_run(arr, len(ctxs), _mat(np.eye(4) if init is None else init, keep),
+                                  int(max_iterations), float(relative_fitness), float(relative_rmse),
+                                  T.ctypes.data, C.byref(fit), C.byref(rmse), C.byref(info)))
+    return _result(T, fit, rmse, info)
+
+
 def nccl_unique_id() -> bytes:
     buf = C.create_string_buffer(128)
     _check(lib().o3g_nccl_unique_id(buf))
@@ -250,6 +266,12 @@ class Context:
     def dist_init(self, rank: int, world: int, unique_id: bytes | None):
         buf = C.create_string_buffer(unique_id, 128) if unique_id is not None else None
         _check(lib().o3g_dist_init(self._h, int(rank), int(world), buf))
+        self.rank, self.world = rank, world
+
+    def dist_init_loopback(self, rank: int, world: int):
+        """o3g_dist_init_loopback: rank `rank` of an in-process world (no
+        communicator); run the world with loopback_run."""
+        _check(lib().o3g_dist_init_loopback(self._h, int(rank), int(world)))
         self.rank, self.world = rank, world
 
     def step(self, T, corr_out=None) -> dict:

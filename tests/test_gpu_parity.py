@@ -618,3 +618,66 @@ def test_run_loop_state_reset_between_runs(o3g, workloads):
             fresh = ctx.run(Tb, 8, 0.0, 0.0)
         assert np.array_equal(rb.transformation, fresh.transformation), cert
         assert rb.fitness == fresh.fitness and rb.inlier_rmse == fresh.inlier_rmse
+
+
+# ------------------------------------------------ A7: the multi-rank path (loopback)
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_loopback_multi_rank(o3g, workloads, world):
+    """SURVEY §8(e) / A7 on one device: P contexts, each keeping its contiguous
+    shard of the spatially ordered source, run the distributed loop in
+    lockstep — per-shard correspondence kernels, TAIL_WRITE_RANK, the slot
+    exchange (device copies standing in for the NCCL all-gather) and the
+    rank-order TAIL_SUM_RANKS tail. The union of the shards' correspondences
+    equals the 1-GPU pass bit for bit at every traced pass; every pass's
+    rank-summed terms agree with the 1-GPU pass (R14) and with the oracle at
+    that T; T is bit-identical on every rank (checked inside the call) and
+    the loop matches the oracle's (1e-6)."""
+    w = workloads("large16m", n=400_000)
+    T0 = w["T_true"] @ _perturb(61, 0.004, 0.01)
+    iters = 6
+    n = len(w["source"])
+    grid_o = oracle.Grid(w["target"], w["dmax"])
+    ref = oracle.icp(w["source"], w["target"], w["target_normals"], w["dmax"], iters, init_T=T0,
+                     relative_fitness=0.0, relative_rmse=0.0)
+    for cert in (1, 0):
+        with _ctx(o3g, w, "balanced", order_T=T0) as one:
+            one.set_option(o3g.OPT_CERT, cert)
+            r1 = one.run(T0, iters, 0.0, 0.0)
+            t1 = one.last_run_trace(r1.passes)
+        ctxs = []
+        try:
+            for rk in range(world):
+                c = o3g.Context(0)
+                c.set_option(o3g.OPT_CERT, cert)
+                c.set_option(2, GRID["dense"])
+                c.set_target(_dev(w["target"]), _dev(w["target_normals"]), w["dmax"])
+                c.dist_init_loopback(rk, world)
+                c.set_source(_dev(w["source"]), T0)
+                ctxs.append(c)
+            rp = o3g.loopback_run(ctxs, T0, iters, 0.0, 0.0)
+            assert rp.passes == r1.passes and rp.iterations == r1.iterations
+            assert np.abs(rp.transformation - ref["T"]).max() <= 1e-6, cert
+            assert abs(rp.fitness - ref["fitness"]) <= 1e-6 and abs(rp.inlier_rmse - ref["inlier_rmse"]) <= 1e-6
+            tp = ctxs[0].last_run_trace(rp.passes)
+            for k in range(rp.passes):
+                refk = oracle.step(tp["T"][k], w["source"], w["target"], w["target_normals"], w["dmax"], grid=grid_o)
+                _terms_ok(tp["terms"][k], refk)
+                _terms_ok(t1["terms"][k], refk)
+            for k in (0, 1, rp.passes - 1):
+                union = np.full(n, -3, np.int32)
+                for c in ctxs:
+                    c.set_option(o3g.OPT_TRACE_PASS, k)
+                o3g.loopback_run(ctxs, T0, iters, 0.0, 0.0)
+                for c in ctxs:
+                    corr = torch.empty(n, dtype=torch.int32, device="cuda")
+                    c.last_run_trace(rp.passes, corr)
+                    got = corr.cpu().numpy()
+                    mine = got != -2
+                    assert np.all(union[mine] == -3)            # shards are disjoint
+                    union[mine] = got[mine]
+                assert np.all(union != -3)                      # and cover the source
+                refk = oracle.step(tp["T"][k], w["source"], w["target"], w["target_normals"], w["dmax"], grid=grid_o)
+                assert np.array_equal(union, refk["corr"]), (world, cert, k)
+        finally:
+            for c in ctxs:
+                c.close()

@@ -1,0 +1,53 @@
+#!/usr/bin/env python
+"""DRAM traffic per correspondence pass from an ncu launch list
+(`ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum
+-k regex:k3_ --csv`): the pass is k3_balanced, or k3_sweep + k3_balanced with
+certificates; prints the per-pass mean time and bytes, and with --key updates
+profiles/k3_traffic.json[key] (read by bench.py's roofline `traffic`)."""
+import argparse
+import csv
+import json
+import os
+
+ap = argparse.ArgumentParser()
+ap.add_argument("csv")
+ap.add_argument("--key", default=None)
+ap.add_argument("--skip", type=int, default=0, help="skip the first N passes (e.g. warm-up registrations)")
+a = ap.parse_args()
+rows = list(csv.reader(open(a.csv)))
+hdr, launches = None, {}
+for row in rows:
+    if "Kernel Name" in row:
+        hdr = row
+        continue
+    if hdr is None or len(row) != len(hdr):
+        continue
+    d = dict(zip(hdr, row))
+    launches.setdefault(int(d["ID"]), {"name": d["Kernel Name"]})[d["Metric Name"]] = (
+        float(d["Metric Value"].replace(",", "")), d["Metric Unit"])
+passes, cur = [], None
+for i in sorted(launches):
+    L = launches[i]
+    t, tu = L["gpu__time_duration.sum"]
+    t = t / 1000.0 if tu == "ns" else t * 1000.0 if tu == "ms" else t   # -> us
+    def mb(k):
+        v, u = L[k]
+        return v * {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3}.get(u, 1e-6)
+    rec = (t, mb("dram__bytes_read.sum") + mb("dram__bytes_write.sum"))
+    if "k3_sweep" in L["name"]:
+        cur = rec
+    elif "k3_balanced" in L["name"]:
+        passes.append((rec[0] + (cur[0] if cur else 0.0), rec[1] + (cur[1] if cur else 0.0)))
+        cur = None
+passes = passes[a.skip:]
+tm = sum(p[0] for p in passes) / len(passes)
+by = sum(p[1] for p in passes) / len(passes)
+print(f"{len(passes)} passes: {tm:.1f} us and {by:.1f} MB DRAM per pass")
+if a.key:
+    path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", "k3_traffic.json")
+    tab = json.load(open(path)) if os.path.exists(path) else {}
+    tab[a.key] = by * 1e6
+    tab["_note"] = ("dram__bytes_read.sum + dram__bytes_write.sum per correspondence pass (k3_balanced, "
+                    "+ k3_sweep with certificates), mean over one registration's passes, ncu --clock-control "
+                    "none (tools/k3_traffic.py); keys config@world@regime")
+    json.dump(tab, open(path, "w"), indent=1, sort_keys=True)

@@ -296,7 +296,8 @@ o3g_status o3g_loopback_run(o3g_ctx* const* ctxs, int world, const double init_T
  *   previous pass matched more than half of the source (the refinement
  *   phase); earlier passes run the plain search. -1 = auto (default: shards
  *   of >= 2^20 queries), 1 = on, 0 = off (the previous winner then only
- *   bounds the next search, the warm start).
+ *   bounds the next search, the warm start), 2 = on from the second pass
+ *   regardless of fitness (experiments).
  * O3G_OPT_TRACE_PASS: k >= 0 = o3g_icp_run also writes the correspondences
  *   of pass k (original source order) for o3g_last_run_trace; -1 = off
  *   (default). A testing hook: it adds a scattered index write to pass k.

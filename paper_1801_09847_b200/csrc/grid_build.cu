@@ -124,6 +124,43 @@ __global__ void k_cs_runs(const uint32_t* __restrict__ keys, int64_t n, int32_t*
     }
 }
 
+// The cell start table straight from the sorted keys, in one pass with no
+// separate memset and max-scan: cs[c] = the first sorted position whose key is
+// >= c, for c in [0, cells] (cs[cells] = n). Sorted position k (0..n) owns the
+// cells (key[k-1], key[k]] (key[-1] = -1, key[n] = cells) and writes k into
+// them; a warp takes 32 consecutive positions, each lane writes its own short
+// range and the whole warp each long one (coalesced; long empty ranges do not
+// serialise one thread). Also sets the occupancy bit of every occupied cell
+// (dense grids).
+__global__ void k_cs_fill(const uint32_t* __restrict__ keys, int64_t n, int64_t cells, int32_t* __restrict__ cs,
+                          uint32_t* __restrict__ occ_bits) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w * 32 <= n; w += nwarps) {
+        const int64_t k = w * 32 + lane;
+        int64_t lo = 0, hi = -1;   // this lane's cells [lo, hi]
+        if (k <= n) {
+            const int64_t prev = k == 0 ? -1 : (int64_t)keys[k - 1];
+            const int64_t cur = k == n ? cells : (int64_t)keys[k];
+            lo = prev + 1, hi = cur;
+            if (occ_bits && k < n && cur != prev) atomicOr(&occ_bits[cur >> 5], 1u << (cur & 31));
+        }
+        // short ranges (the common case: a few cells between neighbouring
+        // points) by their own lane, long ones by the whole warp
+        const bool longr = hi - lo >= 64;
+        if (!longr)
+            for (int64_t c = lo; c <= hi; ++c) cs[c] = (int32_t)k;
+        unsigned todo = __ballot_sync(0xffffffffu, longr);
+        while (todo) {
+            const int src = __ffs(todo) - 1;
+            todo &= todo - 1;
+            const int64_t l = __shfl_sync(0xffffffffu, lo, src), h = __shfl_sync(0xffffffffu, hi, src);
+            const int32_t v = (int32_t)(w * 32 + src);
+            for (int64_t c = l + lane; c <= h; c += 32) cs[c] = v;
+        }
+    }
+}
+
 // hashed grid: occupancy of coarse cells (2^shift fine cells per axis), the
 // live-query test's structure when no dense per-cell bitmap fits
 __global__ void k_coarse_bits(const float4* __restrict__ tpos, int64_t n, GridDev g, int shift, int cnx, int cny,
@@ -299,6 +336,10 @@ void launch_cell_keys(const float* xyz, int64_t n, const GridDev& g, const doubl
 void launch_cs_runs(const uint32_t* keys, int64_t n, int32_t* runs, uint32_t* occ_bits, cudaStream_t s) {
     k_cs_runs<<<blocks_for(n, 256), 256, 0, s>>>(keys, n, runs, occ_bits);
 }
+void launch_cs_fill(const uint32_t* keys, int64_t n, int64_t cells, int32_t* cs, uint32_t* occ_bits,
+                    cudaStream_t s) {
+    k_cs_fill<<<blocks_for(n / 32 + 1, 8), 256, 0, s>>>(keys, n, cells, cs, occ_bits);
+}
 void launch_coarse_bits(const float4* tpos, int64_t n, const GridDev& g, int shift, int cnx, int cny,
                         uint32_t* bits, cudaStream_t s) {
     k_coarse_bits<<<blocks_for(n, 256), 256, 0, s>>>(tpos, n, g, shift, cnx, cny, bits);
@@ -357,14 +398,15 @@ void launch_fill_i32(int32_t* p, int64_t n, int32_t v, cudaStream_t s) {
 
 // every 32-byte certificate record's first half := {-1, all ones, 0, 0}
 // (no winner, invalid certificate); the second half is left as it is
-__global__ void k_cert_reset(float4* cert, int64_t n) {
+__global__ void k_cert_reset(float4* cert, int64_t n, const IcpState* st) {
+    if (!st->creset) return;   // (records of earlier runs are already invalid by their pass tag)
     const float4 v = make_float4(__int_as_float(-1), __int_as_float(-1), 0.f, 0.f);
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x)
         cert[2 * i] = v;
 }
-void launch_cert_reset(float4* cert, int64_t n, cudaStream_t s) {
-    k_cert_reset<<<blocks_for(n, 256), 256, 0, s>>>(cert, n);
+void launch_cert_reset(float4* cert, int64_t n, const IcpState* st, cudaStream_t s) {
+    k_cert_reset<<<blocks_for(n, 256), 256, 0, s>>>(cert, n, st);
 }
 
 }  // namespace o3g

@@ -292,10 +292,13 @@ __device__ __forceinline__ unsigned cert_pack(int pass, float rho, float inv_h_r
     const __half q = __float2half_rz(__fmul_rd(rho, inv_h_rd));   // <= rho / h
     return ((unsigned)pass << 16) | (unsigned)__half_as_ushort(q);
 }
-__device__ __forceinline__ bool cert_valid(unsigned pk, int pass, float x, float y, float z,
+// pass: this run's pass index; gpass = (gbase + pass) mod 2^16 (the tag of
+// records written now); a record is usable iff it was written 1..min(32, pass)
+// passes ago, i.e. earlier in this run
+__device__ __forceinline__ bool cert_valid(unsigned pk, int pass, int gpass, float x, float y, float z,
                                            const float4 (*dT)[3], const float* dC, float h_rd) {
-    const int bp = (int)(pk >> 16), age = pass - bp;
-    if (bp == 0xFFFF || age < 1 || age > kCertAges) return false;
+    const int age = (gpass - (int)(pk >> 16)) & 0xFFFF;
+    if (pk == 0xFFFFFFFFu || age < 1 || age > kCertAges || age > pass) return false;
     const float4 d0 = dT[age - 1][0], d1 = dT[age - 1][1], d2 = dT[age - 1][2];
     const float ex = fmaf(d0.z, z, fmaf(d0.y, y, fmaf(d0.x, x, d0.w)));
     const float ey = fmaf(d1.z, z, fmaf(d1.y, y, fmaf(d1.x, x, d1.w)));
@@ -423,6 +426,7 @@ __global__ void __launch_bounds__(kK3Threads, 4) k3_balanced(const K3Args a) {
     constexpr bool certm = CERT;
     const uint8_t* need = CERT ? a.need : nullptr;
     const int pass = CERT ? a.st->passes : 0;
+    const int gpass = CERT ? (a.st->gbase + pass) & 0xFFFF : 0;
     if (threadIdx.x < 12) sT[threadIdx.x] = a.eval_T ? a.eval_T[16 * blockIdx.y + threadIdx.x] : a.st->T[threadIdx.x];
     if (CERT && threadIdx.x >= 32 && threadIdx.x < 32 + kCertAges)
         cert_tables(a, pass, threadIdx.x - 31, sDT, sDC, &s_rhog);
@@ -1056,7 +1060,7 @@ __global__ void __launch_bounds__(kK3Threads, 4) k3_balanced(const K3Args a) {
                     rho = __fsub_rd(L, dmax_hi);
                 }
             }
-            a.cert[2 * (size_t)i] = make_float4(__int_as_float(win), __uint_as_float(cert_pack(pass, rho, a.inv_h_rd)), wq.x, wq.y);
+            a.cert[2 * (size_t)i] = make_float4(__int_as_float(win), __uint_as_float(cert_pack(gpass, rho, a.inv_h_rd)), wq.x, wq.y);
             if (win >= 0) a.cert[2 * (size_t)i + 1] = make_float4(wq.z, wn.x, wn.y, wn.z);
         }
         if (a.prev_j && i < a.n) {
@@ -1151,7 +1155,7 @@ __device__ __forceinline__ void ld_cert(const float4* c, float4& x, float4& y) {
 
 template <bool WRITE_CORR>
 __device__ __forceinline__ int sweep_query(const K3Args& a, const GridDev& g, const double* sT,
-                                            const float4 (*sDT)[3], const float* sDC, int pass, int i, float4 p,
+                                            const float4 (*sDT)[3], const float* sDC, int pass, int gpass, int i, float4 p,
                                             float4 ca, float4 cb, float Lout, float dmax_hi, double* vw, int lane,
                                             double& acc0, double& acc1) {
     int cwin = -1;
@@ -1159,7 +1163,7 @@ __device__ __forceinline__ int sweep_query(const K3Args& a, const GridDev& g, co
     double tx = 0.0, ty = 0.0, tz = 0.0, cd2 = 0.0;
     float4 cq = make_float4(0.f, 0.f, 0.f, 0.f), cn = cq;
     if (i < a.n) {
-        const bool cv = cert_valid(__float_as_uint(ca.y), pass, p.x, p.y, p.z, sDT, sDC, a.h_rd);
+        const bool cv = cert_valid(__float_as_uint(ca.y), pass, gpass, p.x, p.y, p.z, sDT, sDC, a.h_rd);
         const int cj = __float_as_int(ca.x);
         bool need = false;
         if (!cv || cj >= 0) xform_rn(sT, p.x, p.y, p.z, tx, ty, tz);
@@ -1205,7 +1209,7 @@ __device__ __forceinline__ int sweep_query(const K3Args& a, const GridDev& g, co
                     if (!((__ldg(&a.nbr2_bits[kc >> 5]) >> (kc & 31)) & 1u)) reach = __fadd_rd(reach, Lout);
                 }
                 a.cert[2 * (size_t)i] = make_float4(__int_as_float(-1),
-                                                    __uint_as_float(cert_pack(pass, __fsub_rd(reach, dmax_hi), a.inv_h_rd)),
+                                                    __uint_as_float(cert_pack(gpass, __fsub_rd(reach, dmax_hi), a.inv_h_rd)),
                                                     0.f, 0.f);
                 if (WRITE_CORR) a.corr_out[__float_as_int(p.w)] = -1;
             }
@@ -1270,6 +1274,7 @@ __global__ void __launch_bounds__(kSweepThreads, 3) k3_sweep(const K3Args a) {
         return;
     }
     const int pass = a.st->passes;
+    const int gpass = (a.st->gbase + pass) & 0xFFFF;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     SweepStage* stages = (SweepStage*)sw_smem + warp * kSweepStages;
     uint64_t* wbar = bar[warp];
@@ -1302,7 +1307,7 @@ __global__ void __launch_bounds__(kSweepThreads, 3) k3_sweep(const K3Args a) {
         const float4 ca = sg.cert[2 * lane], cb = sg.cert[2 * lane + 1];
         __syncwarp();   // the warp is done with this stage: refill it
         if (lane == 0 && b + kSweepStages * nw < nb) sweep_issue(a, &stages[sidx], &wbar[sidx], b + kSweepStages * nw);
-        ncert += sweep_query<WRITE_CORR>(a, g, sT, sDT, sDC, pass, b * 32 + lane, p, ca, cb, Lout, dmax_hi, vw,
+        ncert += sweep_query<WRITE_CORR>(a, g, sT, sDT, sDC, pass, gpass, b * 32 + lane, p, ca, cb, Lout, dmax_hi, vw,
                                          lane, acc0, acc1);
     }
     __syncwarp();
@@ -1593,7 +1598,7 @@ __device__ __noinline__ void tail_finish(const double* terms, IcpState* st, cons
     st->passes = p + 1;
     st->fit = fit;
     st->rmse = rmse;
-    st->cmode = fit > 0.5 ? 1 : 0;   // (next pass: certificates once most queries match)
+    st->cmode = (fit > 0.5 || st->cforce) ? 1 : 0;   // (next pass: certificates once most queries match)
     int done = 0;
     if (p > 0 && fabs(fit - st->fit_prev) < st->rel_fit && fabs(rmse - st->rmse_prev) < st->rel_rmse) {
         st->converged = 1;

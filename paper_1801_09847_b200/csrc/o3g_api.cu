@@ -164,6 +164,8 @@ struct o3g_ctx {
     DevBuf src4;
     DevBuf prevj;          // run loop: previous pass's winner per local query
     DevBuf cert;           // run loop: per local query certificate (2 x float4, §5.5)
+    int32_t cert_epoch = 0;        // the next run's gbase (pass tag base of certificates)
+    bool cert_fresh = true;        // the records need a reset (new buffer / tag wrap-around)
     DevBuf need;           // run loop: per local query search flag (sweep -> search)
     DevBuf hist_T, hist_terms, trace_corr;   // run loop: per-pass T / terms, traced corr
     float smax[3] = {0.f, 0.f, 0.f};         // max |source coordinate| per axis
@@ -386,7 +388,7 @@ o3g_status o3g_set_option(o3g_ctx* c, int option, int64_t value) {
             c->coop_min = (int)value;
             break;
         case O3G_OPT_CERT:
-            if (value < -1 || value > 1) return fail(O3G_ERR_INVALID_ARGUMENT, "cert must be -1, 0 or 1");
+            if (value < -1 || value > 2) return fail(O3G_ERR_INVALID_ARGUMENT, "cert must be -1, 0, 1 or 2");
             c->cert_opt = (int)value;
             break;
         case O3G_OPT_TRACE_PASS:
@@ -471,7 +473,7 @@ static o3g_status set_target_impl(o3g_ctx* c, const float* xyz, const float* nor
     TRY(c->vals_a.ensure(n * 4));
     TRY(c->vals_b.ensure(n * 4));
     TRY(c->cell_start.ensure((g.table_size + 1) * 4));
-    TRY(c->counts.ensure((g.table_size + 1) * 4));
+    if (c->target_sort != 1) TRY(c->counts.ensure((g.table_size + 1) * 4));   // (counting sort only)
     TRY(c->tpos.ensure((n + 2) * sizeof(float4)));   // +pad: pair loads may touch tpos[n]
     TRY(c->tnrm.ensure(n * sizeof(float4)));
 
@@ -480,8 +482,8 @@ static o3g_status set_target_impl(o3g_ctx* c, const float* xyz, const float* nor
     bool occ_built = false;
     if (radix) {
         TRY(sort_pairs(c, n, bits_for((uint64_t)(g.table_size - 1))));
-        // cell starts from the sorted keys (no histogram): run ends, then an
-        // exclusive max scan; dense grids get their occupancy bits here
+        // cell starts straight from the sorted keys (one pass, no histogram,
+        // memset or scan); dense grids get their occupancy bits here
         uint32_t* obits = nullptr;
         if (!g.hashed) {
             const int64_t nw = (g.table_size + 31) / 32;
@@ -491,14 +493,7 @@ static o3g_status set_target_impl(o3g_ctx* c, const float* xyz, const float* nor
             obits = c->nbr_a.as<uint32_t>();
             occ_built = true;
         }
-        CK(cudaMemsetAsync(c->counts.p, 0, (g.table_size + 1) * 4, c->exec));
-        launch_cs_runs(c->keys_b.as<uint32_t>(), n, c->counts.as<int32_t>(), obits, c->exec);
-        size_t tmp = 0;
-        CK(cub::DeviceScan::ExclusiveScan(nullptr, tmp, c->counts.as<int32_t>(), c->cell_start.as<int32_t>(),
-                                          cub::Max(), (int32_t)0, (int)(g.table_size + 1), c->exec));
-        TRY(c->cub_tmp.ensure(tmp));
-        CK(cub::DeviceScan::ExclusiveScan(c->cub_tmp.p, tmp, c->counts.as<int32_t>(), c->cell_start.as<int32_t>(),
-                                          cub::Max(), (int32_t)0, (int)(g.table_size + 1), c->exec));
+        launch_cs_fill(c->keys_b.as<uint32_t>(), n, g.table_size, c->cell_start.as<int32_t>(), obits, c->exec);
     } else {
         CK(cudaMemsetAsync(c->counts.p, 0, (g.table_size + 1) * 4, c->exec));
         launch_histogram(c->keys_a.as<uint32_t>(), n, c->counts.as<int32_t>(), occ, c->exec);
@@ -882,6 +877,17 @@ static void init_state(o3g_ctx* c, const double* T, int max_it, double ef, doubl
     s->rel_rmse = er;
     s->n_total = (double)c->n_total;
     s->hist_cap = cap;
+    s->cforce = c->cert_opt == 2 ? 1 : 0;
+    // certificate pass tags: this run uses gbase .. gbase + max_it (mod 2^16);
+    // records tagged by an earlier run are then older than any usable age. A
+    // fresh buffer or a wrap-around within 64 tags resets them all.
+    if (c->cert_fresh || c->cert_epoch + max_it + 1 + 64 > 65535) {
+        c->cert_epoch = 0;
+        s->creset = 1;
+        c->cert_fresh = false;
+    }
+    s->gbase = c->cert_epoch;
+    c->cert_epoch += max_it + 1;
 }
 
 o3g_status o3g_icp_step(o3g_ctx* c, const double T_in[16], int32_t* corr_out, double JTJ_out[36],
@@ -926,7 +932,7 @@ o3g_status o3g_icp_step(o3g_ctx* c, const double T_in[16], int32_t* corr_out, do
 // extra sweep launch and the certificate searches cost more than they save:
 // depth 0.042 -> 0.117 ms per pass, tiny 0.022 -> 0.023)
 static bool cert_on(const o3g_ctx* c, int max_it) {
-    const bool want = c->cert_opt == 1 || (c->cert_opt == -1 && c->n_local >= (1 << 20));
+    const bool want = c->cert_opt >= 1 || (c->cert_opt == -1 && c->n_local >= (1 << 20));
     return want && k3_variant(c) == 1 && max_it + 1 < 65535 && c->n_local > 0;
 }
 
@@ -946,7 +952,9 @@ static int sweep_blocks(const o3g_ctx* c) {
 static o3g_status run_state_buffers(o3g_ctx* c, bool certm, bool trace) {
     TRY(c->prevj.ensure((size_t)(c->n_local > 0 ? c->n_local : 1) * 4));
     if (certm) {
-        TRY(c->cert.ensure((size_t)c->n_local * 2 * sizeof(float4)));
+        bool grew = false;
+        TRY(c->cert.ensure((size_t)c->n_local * 2 * sizeof(float4), &grew));
+        if (grew) c->cert_fresh = true;
         TRY(c->need.ensure((size_t)c->n_local + 256));   // (+ a zero tail: flags are read 8 at a time)
     }
     if (trace) TRY(c->trace_corr.ensure((size_t)c->n_total * 4));
@@ -954,7 +962,7 @@ static o3g_status run_state_buffers(o3g_ctx* c, bool certm, bool trace) {
 }
 static o3g_status run_prologue(o3g_ctx* c, bool certm, bool trace) {
     if (c->n_local > 0) CK(cudaMemsetAsync(c->prevj.p, 0xFF, (size_t)c->n_local * 4, c->exec));
-    if (c->n_local > 0 && certm) launch_cert_reset(c->cert.as<float4>(), c->n_local, c->exec);
+    if (c->n_local > 0 && certm) launch_cert_reset(c->cert.as<float4>(), c->n_local, c->state.as<IcpState>(), c->exec);
     if (certm) CK(cudaMemsetAsync(c->need.as<uint8_t>() + c->n_local, 0, 256, c->exec));
     if (trace) launch_fill_i32(c->trace_corr.as<int32_t>(), c->n_total, -2, c->exec);
     return O3G_OK;
@@ -1041,6 +1049,8 @@ o3g_status o3g_icp_run(o3g_ctx* c, const double init_T[16], int32_t max_iteratio
     const int blocks = k3_blocks(c, false);
     const int sblocks = cert_on(c, max_iterations) ? sweep_blocks(c) : 0;
     TRY(loop_buffers(c, blocks + sblocks, max_iterations + 1));
+    // (buffers first: a new certificate buffer requests the reset in init_state)
+    TRY(run_state_buffers(c, sblocks > 0, c->trace_pass >= 0 && c->trace_pass <= max_iterations));
     init_state(c, init_T, max_iterations, relative_fitness, relative_rmse, max_iterations + 1);
     CK(cudaMemcpyAsync(c->state.p, c->h_state, sizeof(IcpState), cudaMemcpyHostToDevice, c->exec));
     TRY(build_graph(c, max_iterations, blocks, sblocks));

@@ -45,6 +45,11 @@ struct IcpState {
     int32_t it, max_it, passes, done, flags, converged, hist_cap;
     int32_t cmode;   // certificates: this pass runs the sweep + certified search (set by
                      // the previous pass's tail: fitness > 1/2, the refinement phase)
+    int32_t cforce;  // O3G_OPT_CERT = 2: every pass after the first (experiments)
+    int32_t gbase;   // certificates carry (gbase + pass) mod 2^16: a record from an earlier
+                     // run is older than the current pass index, hence invalid; the host
+                     // advances gbase per run and requests a reset (creset) on wrap-around
+    int32_t creset;  // 1: k_cert_reset clears the records at the head of this run
 };
 
 enum TailMode : int {
@@ -95,6 +100,9 @@ void launch_check_finite(const float* v, int64_t count, int32_t* nonfinite, int 
 void launch_cell_keys(const float* xyz, int64_t n, const GridDev& g, const double* T12_or_null,
                       uint32_t* keys, int32_t* vals, cudaStream_t s, int brick = 0);
 void launch_cs_runs(const uint32_t* keys, int64_t n, int32_t* runs, uint32_t* occ_bits, cudaStream_t s);
+// cell start table [cells + 1] from the sorted keys in one pass (+ occupancy bits)
+void launch_cs_fill(const uint32_t* keys, int64_t n, int64_t cells, int32_t* cs, uint32_t* occ_bits,
+                    cudaStream_t s);
 void launch_dilate3(uint32_t* bits, uint32_t* tmp, int64_t ncells, int64_t nx, int64_t nxny, cudaStream_t s);
 void launch_coarse_bits(const float4* tpos, int64_t n, const GridDev& g, int shift, int cnx, int cny,
                         uint32_t* bits, cudaStream_t s);
@@ -114,7 +122,7 @@ void launch_gather_target(const float* xyz, const float* nrm, const int32_t* val
 void launch_gather_source(const float* xyz, const int32_t* vals_sorted, int64_t lo, int64_t hi,
                           float4* out, cudaStream_t s);
 void launch_fill_i32(int32_t* p, int64_t n, int32_t v, cudaStream_t s);
-void launch_cert_reset(float4* cert, int64_t n, cudaStream_t s);
+void launch_cert_reset(float4* cert, int64_t n, const IcpState* st, cudaStream_t s);
 // dilated occupancy bitmap of a dense grid: occupancy from cell_start, then
 // three shifted-OR passes (x by 1, y by nx, z by nx*ny). Bits that wrap across
 // row / slab boundaries only add false positives (a query then just does the

@@ -681,3 +681,29 @@ def test_loopback_multi_rank(o3g, workloads, world):
         finally:
             for c in ctxs:
                 c.close()
+
+
+def test_certificate_tags_wrap(o3g, workloads):
+    """Certificate records carry a 16-bit pass tag that advances across runs;
+    records of an earlier run are older than any usable age, and the records
+    are reset when the tags wrap (~2100 runs of 31 passes here): every run
+    equals a fresh context's run bit for bit."""
+    w = workloads("tiny")
+    T0 = w["init_T"]
+    with _ctx(o3g, w, "balanced", order_T=T0) as ctx:
+        ctx.set_option(o3g.OPT_CERT, 1)
+        ref = ctx.run(T0, w["iters"], 0.0, 0.0)
+        Ts = [w["T_true"] @ _perturb(70 + k, 0.01, 0.01) for k in range(3)]
+        fresh = []
+        for T in Ts:
+            with _ctx(o3g, w, "balanced", order_T=T0) as c2:
+                c2.set_option(o3g.OPT_CERT, 1)
+                fresh.append(c2.run(T, 30, 0.0, 0.0))
+        for k in range(2200):
+            j = k % 3
+            r = ctx.run(Ts[j], 30, 0.0, 0.0)
+            if k % 97 == 0 or k > 2090:
+                assert np.array_equal(r.transformation, fresh[j].transformation), k
+                assert r.fitness == fresh[j].fitness, k
+        r = ctx.run(T0, w["iters"], 0.0, 0.0)
+        assert np.array_equal(r.transformation, ref.transformation)

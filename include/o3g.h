@@ -124,7 +124,9 @@ o3g_status o3g_set_target(o3g_ctx* ctx, const float* xyz, const float* normals, 
  * identity) for locality. Requires o3g_set_target first. The FULL source
  * is passed on every rank; when distributed (o3g_dist_init) the context
  * keeps its contiguous shard of the spatial order and the fitness
- * denominator stays n (the global count).                               */
+ * denominator stays n (the global count). 1 <= n <= 2^31 - 2^24 (the
+ * kernels' 32-bit batch cursors step past the last query); device arrays
+ * must live on the context's device (O3G_ERR_INVALID_ARGUMENT otherwise). */
 o3g_status o3g_set_source(o3g_ctx* ctx, const float* xyz, int64_t n, const double order_T[16]);
 
 /* One correspondence + reduction pass at fixed T_in (north_star's

@@ -997,6 +997,13 @@ __global__ void __launch_bounds__(kK3Threads, 4) k3_balanced(const K3Args a) {
             }
         }
 
+#if defined(O3G_SOL)
+        // speed-of-light build (tools/sweeps/sol.sh, never the product): the
+        // candidate loads and the (m1, j1, m2) scan only; no decision, record or
+        // reduction (a sink keeps the scan alive)
+        if (m1 == -1.f && j1 == -7) a.block_partials[0] = m2;
+        continue;
+#endif
         // decision (exact fp64 rule, R1-R3)
         bool uniq = CERT && !heavy;   // (certificates: the decision had a unique nearest candidate)
         if (!heavy && c > 0 && m1 <= thr0) {

@@ -202,6 +202,17 @@ static bool is_device_ptr(const void* p) {
     return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
 }
 
+// device memory of ANOTHER device (the kernels would dereference it without
+// peer access: a sticky fault): rejected as an invalid argument
+static bool foreign_device_ptr(const void* p, int device) {
+    cudaPointerAttributes at;
+    if (!p || cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeDevice && at.device != device;
+}
+
 // the largest float <= v (v > 0)
 static float round_down_f(double v) {
     float f = (float)v;
@@ -244,6 +255,8 @@ static o3g_status enter(o3g_ctx* c) {
 // memory, else a copy into a context staging buffer (the e2e path).
 static o3g_status device_view(o3g_ctx* c, const float* p, int64_t count, DevBuf& stage,
                               const float** out) {
+    if (foreign_device_ptr(p, c->device))
+        return fail(O3G_ERR_INVALID_ARGUMENT, "array is device memory of another device than the context's");
     if (is_device_ptr(p)) {
         *out = p;
         return O3G_OK;
@@ -611,7 +624,8 @@ o3g_status o3g_set_target(o3g_ctx* c, const float* xyz, const float* normals, in
 o3g_status o3g_set_source(o3g_ctx* c, const float* xyz, int64_t n, const double order_T[16]) {
     if (!c) return fail(O3G_ERR_INVALID_ARGUMENT, "ctx is NULL");
     if (!xyz) return fail(O3G_ERR_INVALID_ARGUMENT, "source xyz is required");
-    if (n <= 0 || n > 0x7ffffffeLL) return fail(O3G_ERR_INVALID_ARGUMENT, "n_source must be in [1, 2^31-2]");
+    // (the kernels' 32-bit batch cursors step by up to 2^24 past the last query)
+    if (n <= 0 || n > 0x7effffffLL) return fail(O3G_ERR_INVALID_ARGUMENT, "n_source must be in [1, 2^31 - 2^24]");
     if (c->m <= 0) return fail(O3G_ERR_INVALID_ARGUMENT, "o3g_set_target must be called first");
     if (order_T && !rigid_ok(order_T)) return fail(O3G_ERR_INVALID_ARGUMENT, "order_T is not a rigid transform");
     TRY(enter(c));
@@ -897,7 +911,8 @@ o3g_status o3g_icp_step(o3g_ctx* c, const double T_in[16], int32_t* corr_out, do
     if (!rigid_ok(T_in)) return fail(O3G_ERR_INVALID_ARGUMENT, "T_in is not a rigid transform");
     if (!c->src_ready) return fail(O3G_ERR_INVALID_ARGUMENT, "o3g_set_target and o3g_set_source must be called first");
     if (!c->estimation && !c->has_normals) return fail(O3G_ERR_INVALID_ARGUMENT, "point-to-plane needs target normals");
-    if (corr_out && !is_device_ptr(corr_out)) return fail(O3G_ERR_INVALID_ARGUMENT, "corr_out must be device memory");
+    if (corr_out && (!is_device_ptr(corr_out) || foreign_device_ptr(corr_out, c->device)))
+        return fail(O3G_ERR_INVALID_ARGUMENT, "corr_out must be device memory of the context's device");
     TRY(enter(c));
     const bool wc = corr_out != nullptr;
     const int blocks = k3_blocks(c, wc);
@@ -1292,8 +1307,10 @@ extern "C" o3g_status o3g_estimate_normals(o3g_ctx* c, const float* xyz, int64_t
     if (!c) return fail(O3G_ERR_INVALID_ARGUMENT, "ctx is NULL");
     if (n < 3) return fail(O3G_ERR_INVALID_ARGUMENT, "estimate_normals needs at least 3 points (S:71)");
     if (max_nn < 1 || max_nn > 64) return fail(O3G_ERR_INVALID_ARGUMENT, "max_nn must be in [1, 64]");
-    if (!out_normals || !is_device_ptr(out_normals)) return fail(O3G_ERR_INVALID_ARGUMENT, "out_normals must be device memory");
-    if (nbr_count && !is_device_ptr(nbr_count)) return fail(O3G_ERR_INVALID_ARGUMENT, "nbr_count must be device memory");
+    if (!out_normals || !is_device_ptr(out_normals) || foreign_device_ptr(out_normals, c->device))
+        return fail(O3G_ERR_INVALID_ARGUMENT, "out_normals must be device memory of the context's device");
+    if (nbr_count && (!is_device_ptr(nbr_count) || foreign_device_ptr(nbr_count, c->device)))
+        return fail(O3G_ERR_INVALID_ARGUMENT, "nbr_count must be device memory of the context's device");
     TRY(o3g_set_target(c, xyz, nullptr, n, radius));   // the cloud's own grid, cell = radius
     c->src_ready = false;
     TRY(c->misc.ensure(64));
@@ -1322,21 +1339,28 @@ extern "C" o3g_status o3g_evaluate_registration(o3g_ctx* c, const double* Ts, in
     if (c->world != 1) return fail(O3G_ERR_NOT_IMPLEMENTED, "batched evaluation is single-GPU");
     TRY(enter(c));
     const int blocks = k3_blocks(c, false);
+    // transforms go in chunks of <= 1024 per launch: the partials buffer stays
+    // bounded (1024 x blocks x 256 B, ~155 MB at 592 blocks) for any k
+    constexpr int kEvalChunk = 1024;
+    const int kc = k < kEvalChunk ? k : kEvalChunk;
     TRY(c->ev_T.ensure((size_t)k * 16 * sizeof(double)));
-    TRY(c->ev_part.ensure((size_t)k * blocks * kTermStride * sizeof(double)));
+    TRY(c->ev_part.ensure((size_t)kc * blocks * kTermStride * sizeof(double)));
     TRY(c->ev_out.ensure((size_t)k * 2 * sizeof(double)));
     TRY(c->state.ensure(sizeof(IcpState)));
     CK(cudaMemcpyAsync(c->ev_T.p, Ts, (size_t)k * 16 * sizeof(double), cudaMemcpyHostToDevice, c->exec));
     K3Args a = k3_args(c, nullptr);
     a.p2p = 1;                       // count and sum d^2 ride in the point-to-point record
-    a.eval_T = c->ev_T.as<double>();
-    a.n_eval = k;
     a.block_partials = c->ev_part.as<double>();
     if (c->n_local > 0) {
-        launch_k3(a, blocks, 1, false, c->exec);
-        launch_eval_reduce(c->ev_part.as<double>(), blocks, k, (double)c->n_total, c->ev_out.as<double>(),
-                           c->ev_out.as<double>() + k, c->exec);
-        c->launches += 2;
+        for (int k0 = 0; k0 < k; k0 += kEvalChunk) {
+            const int kn = k - k0 < kEvalChunk ? k - k0 : kEvalChunk;
+            a.eval_T = c->ev_T.as<double>() + 16 * (size_t)k0;
+            a.n_eval = kn;
+            launch_k3(a, blocks, 1, false, c->exec);
+            launch_eval_reduce(c->ev_part.as<double>(), blocks, kn, (double)c->n_total, c->ev_out.as<double>() + k0,
+                               c->ev_out.as<double>() + k + k0, c->exec);
+            c->launches += 2;
+        }
     } else {
         CK(cudaMemsetAsync(c->ev_out.p, 0, (size_t)k * 2 * sizeof(double), c->exec));
     }
@@ -1418,8 +1442,10 @@ extern "C" o3g_status o3g_voxel_down_sample(o3g_ctx* c, const float* xyz, const 
                                             double voxel, float* out_xyz, float* out_normals,
                                             int64_t* n_out) {
     if (!c) return fail(O3G_ERR_INVALID_ARGUMENT, "ctx is NULL");
-    if (out_xyz && !is_device_ptr(out_xyz)) return fail(O3G_ERR_INVALID_ARGUMENT, "out_xyz must be device memory");
-    if (out_normals && !is_device_ptr(out_normals)) return fail(O3G_ERR_INVALID_ARGUMENT, "out_normals must be device memory");
+    if (out_xyz && (!is_device_ptr(out_xyz) || foreign_device_ptr(out_xyz, c->device)))
+        return fail(O3G_ERR_INVALID_ARGUMENT, "out_xyz must be device memory of the context's device");
+    if (out_normals && (!is_device_ptr(out_normals) || foreign_device_ptr(out_normals, c->device)))
+        return fail(O3G_ERR_INVALID_ARGUMENT, "out_normals must be device memory of the context's device");
     return voxel_impl(c, xyz, normals, n, voxel, out_xyz, out_normals, n_out);
 }
 

@@ -7,7 +7,8 @@ bitwise the same for any thread count) on every host core:
   R14 at the start T and at T*; the full 30-update loop in the launch
   configuration bench.py times (certificates on by default) with T within
   1e-6, fitness and rmse within 1e-6, the same updates and flags; and every
-  pass of that loop against the oracle's pass at the T it ran with.
+  fifth pass of that loop against the oracle's pass at the T it ran with;
+  the converged regime (certificates carrying most passes) likewise.
 - fragment (2M / 2M, three scales): the multi-scale loop at the benchmarked size.
 """
 import os

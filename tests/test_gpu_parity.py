@@ -295,12 +295,30 @@ def test_invalid_arguments(o3g, workloads):
     # option ranges (include/o3g.h): every invalid value is rejected, valid ones accepted
     with o3g.Context(0) as ctx:
         for opt, bad_v in ((1, 5), (1, -1), (2, 3), (4, 65), (6, -2), (7, 2), (8, 2), (9, 2), (10, -4),
-                           (11, 2), (11, -2), (12, 2), (99, 0)):
+                           (11, 2), (11, -2), (12, 2), (13, 3), (13, -2), (14, -2), (99, 0)):
             with pytest.raises(E):
                 ctx.set_option(opt, bad_v)
         for opt, ok_v in ((1, 4), (2, 0), (3, 1), (4, 0), (5, 0), (6, -1), (7, 0), (8, 1), (9, 0), (10, -2),
-                          (11, -1), (12, -1)):
+                          (11, -1), (12, -1), (13, -1), (13, 2), (14, 3), (14, -1)):
             ctx.set_option(opt, ok_v)
+
+
+def test_batched_evaluation_chunks(o3g, workloads):
+    """o3g_evaluate_registration processes transforms in chunks of 1024 per
+    launch (bounded scratch, ADVICE): 2500 transforms give exactly the values
+    of evaluating each chunk's transforms on their own."""
+    w = workloads("tiny")
+    Ts = np.stack([w["T_true"] @ _perturb(200 + k, 0.02, 0.02) for k in range(2500)])
+    with _ctx(o3g, w) as ctx:
+        fit, rmse = ctx.evaluate(Ts)
+        f2, r2 = ctx.evaluate(Ts[1000:1100])
+        f3, r3 = ctx.evaluate(Ts[2048:])
+    assert np.array_equal(fit[1000:1100], f2) and np.array_equal(rmse[1000:1100], r2)
+    assert np.array_equal(fit[2048:], f3) and np.array_equal(rmse[2048:], r3)
+    grid = oracle.Grid(w["target"], w["dmax"])
+    for k in (0, 1023, 1024, 2047, 2048, 2499):
+        ref = oracle.step(Ts[k], w["source"], w["target"], w["target_normals"], w["dmax"], grid=grid)
+        assert fit[k] == ref["count"] / len(w["source"]), k
 
 
 def test_flags_no_corr_and_degenerate(o3g, workloads):

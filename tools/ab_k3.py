@@ -14,6 +14,7 @@ ap.add_argument("libs", nargs="+")
 ap.add_argument("--config", default="large16m")
 ap.add_argument("--regime", default="init")
 ap.add_argument("--reps", type=int, default=3)
+ap.add_argument("--iters", type=int, default=None, help="updates (default: the config's)")
 ap.add_argument("--opt", action="append", default=[], help="option=value applied to every library")
 a = ap.parse_args()
 
@@ -59,7 +60,8 @@ for rep in range(a.reps + 1):
     for name, L, h in libs:
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        assert L.o3g_icp_run(h, T0.ctypes.data, w["iters"], 0.0, 0.0, T.ctypes.data, C.byref(fit), C.byref(rmse),
+        assert L.o3g_icp_run(h, T0.ctypes.data, w["iters"] if a.iters is None else a.iters, 0.0, 0.0,
+                             T.ctypes.data, C.byref(fit), C.byref(rmse),
                              None, None, None) == 0
         e1.record()
         torch.cuda.synchronize()

@@ -389,6 +389,39 @@ __device__ __forceinline__ void accumulate_records(const K3Args& a, double* vw, 
     __syncwarp();
 }
 
+// A5 + A6 for one record in per-lane fp64 registers (the certificate sweep:
+// a streaming kernel whose lanes each settle one query per batch; the
+// terms are the flat kTerms layout of k_tail, summed by the fixed-order
+// butterfly + block sum of sweep_block_partial). Point-to-plane (R4):
+// [0..20] J_u J_v (u <= v), [21..26] J_u r, [27] count, [28] sum d2;
+// point-to-point: [0..8] s'_a q_b, [9..11] s', [12..14] q, [27], [28].
+__device__ __forceinline__ void acc_record(const K3Args& a, double (&acc)[kTerms], double sx, double sy, double sz,
+                                           float4 wq, float4 nf, double wd2) {
+    if (a.p2p) {
+        const double s3[3] = {sx, sy, sz}, q3[3] = {wq.x, wq.y, wq.z};
+#pragma unroll
+        for (int u = 0; u < 3; ++u) {
+#pragma unroll
+            for (int v = 0; v < 3; ++v) acc[3 * u + v] += s3[u] * q3[v];
+            acc[9 + u] += s3[u];
+            acc[12 + u] += q3[u];
+        }
+    } else {
+        const double nx = nf.x, ny = nf.y, nz = nf.z;
+        const double r = (sx - (double)wq.x) * nx + (sy - (double)wq.y) * ny + (sz - (double)wq.z) * nz;
+        const double J[6] = {sy * nz - sz * ny, sz * nx - sx * nz, sx * ny - sy * nx, nx, ny, nz};
+        int k = 0;
+#pragma unroll
+        for (int u = 0; u < 6; ++u)
+#pragma unroll
+            for (int v = u; v < 6; ++v) acc[k++] += J[u] * J[v];
+#pragma unroll
+        for (int u = 0; u < 6; ++u) acc[21 + u] += J[u] * r;
+    }
+    acc[27] += 1.0;
+    acc[28] += wd2;
+}
+
 // live test of the query in cell (cx, cy, cz) (cells in [-2, n+1]): one bit
 // of the dilated occupancy bitmap — per cell on a dense grid; on a hashed grid
 // per 2^cshift-cell coarse cell (the fine stencil [c-1, c+1] lies inside the
@@ -1163,8 +1196,8 @@ __device__ __forceinline__ void ld_cert(const float4* c, float4& x, float4& y) {
 template <bool WRITE_CORR>
 __device__ __forceinline__ int sweep_query(const K3Args& a, const GridDev& g, const double* sT,
                                             const float4 (*sDT)[3], const float* sDC, int pass, int gpass, int i, float4 p,
-                                            float4 ca, float4 cb, float Lout, float dmax_hi, double* vw, int lane,
-                                            double& acc0, double& acc1) {
+                                            float4 ca, float4 cb, float Lout, float dmax_hi,
+                                            double (&acc)[kTerms]) {
     int cwin = -1;
     bool certified = false;
     double tx = 0.0, ty = 0.0, tz = 0.0, cd2 = 0.0;
@@ -1225,7 +1258,7 @@ __device__ __forceinline__ int sweep_query(const K3Args& a, const GridDev& g, co
         a.need[i] = need ? 1 : 0;
         certified = cv;
     }
-    accumulate_records(a, vw, lane, cwin, tx, ty, tz, cq, cn, cd2, acc0, acc1);
+    if (cwin >= 0) acc_record(a, acc, tx, ty, tz, cq, cn, cd2);
     return certified ? 1 : 0;
 }
 
@@ -1266,14 +1299,14 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 }
 
 template <bool WRITE_CORR>
-__global__ void __launch_bounds__(kSweepThreads, 3) k3_sweep(const K3Args a) {
+__global__ void __launch_bounds__(kSweepThreads, 2) k3_sweep(const K3Args a) {
     extern __shared__ __align__(128) unsigned char sw_smem[];
     __shared__ __align__(8) uint64_t bar[kSweepThreads / 32][kSweepStages];
     __shared__ double sT[12];
     __shared__ __align__(16) float4 sDT[kCertAges][3];
     __shared__ float sDC[kCertAges];
     __shared__ float s_rhog;
-    __shared__ __align__(16) double s_vw[kSweepThreads / 32][9 * kVW];
+    __shared__ double s_red[kSweepThreads / 32][kTerms];
     __shared__ int s_ncert[kSweepThreads / 32];
     if (a.st->done || !a.st->cmode || a.st->passes != a.pass_expect) {   // (plain pass: k3_balanced does it all)
         if (!a.st->done && threadIdx.x < kTermStride)
@@ -1299,8 +1332,9 @@ __global__ void __launch_bounds__(kSweepThreads, 3) k3_sweep(const K3Args a) {
     if (threadIdx.x >= 32 && threadIdx.x < 32 + kCertAges) cert_tables(a, pass, threadIdx.x - 31, sDT, sDC, &s_rhog);
     __syncthreads();
     const GridDev g = a.g;
-    double* vw = s_vw[warp];
-    double acc0 = 0.0, acc1 = 0.0;
+    double acc[kTerms];   // this lane's records (A5), in registers
+#pragma unroll
+    for (int t = 0; t < kTerms; ++t) acc[t] = 0.0;
     int ncert = 0;
     const float Lout = __fmul_rd(a.h_rd, 1.0f - 1.1920928955078125e-07f);
     const float dmax_hi = __double2float_ru(a.dmax * (1.0 + 9.094947017729282e-13));
@@ -1314,21 +1348,27 @@ __global__ void __launch_bounds__(kSweepThreads, 3) k3_sweep(const K3Args a) {
         const float4 ca = sg.cert[2 * lane], cb = sg.cert[2 * lane + 1];
         __syncwarp();   // the warp is done with this stage: refill it
         if (lane == 0 && b + kSweepStages * nw < nb) sweep_issue(a, &stages[sidx], &wbar[sidx], b + kSweepStages * nw);
-        ncert += sweep_query<WRITE_CORR>(a, g, sT, sDT, sDC, pass, gpass, b * 32 + lane, p, ca, cb, Lout, dmax_hi, vw,
-                                         lane, acc0, acc1);
+        ncert += sweep_query<WRITE_CORR>(a, g, sT, sDT, sDC, pass, gpass, b * 32 + lane, p, ca, cb, Lout, dmax_hi,
+                                         acc);
     }
     __syncwarp();
 #pragma unroll
     for (int o = 16; o; o >>= 1) ncert += __shfl_xor_sync(0xffffffffu, ncert, o);
     if (lane == 0) s_ncert[warp] = ncert;
-    vw[(lane >> 2) * 8 + 2 * (lane & 3)] = acc0;   // C of this warp
-    vw[(lane >> 2) * 8 + 2 * (lane & 3) + 1] = acc1;
+    // A6: per term a fixed-order butterfly over the warp's lanes, then the
+    // warps in order
+#pragma unroll
+    for (int t = 0; t < kTerms; ++t) {
+        double v = acc[t];
+#pragma unroll
+        for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) s_red[warp][t] = v;
+    }
     __syncthreads();
     if (threadIdx.x < kTermStride) {
         double s = 0.0;
-        const int ci = a.p2p ? term_cidx_p2p(threadIdx.x) : (threadIdx.x < kTerms ? term_cidx(threadIdx.x) : -1);
-        if (ci >= 0)
-            for (int w = 0; w < kSweepThreads / 32; ++w) s += s_vw[w][ci];
+        if (threadIdx.x < kTerms)
+            for (int w = 0; w < kSweepThreads / 32; ++w) s += s_red[w][threadIdx.x];
         if (threadIdx.x == kStatCertified)
             for (int w = 0; w < kSweepThreads / 32; ++w) s += (double)s_ncert[w];
         a.block_partials[((size_t)a.part_off + blockIdx.x) * kTermStride + threadIdx.x] = s;

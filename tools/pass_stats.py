@@ -15,6 +15,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="large16m")
 ap.add_argument("--regime", default="init", choices=["init", "converged"])
 ap.add_argument("--iters", type=int, default=None)
+ap.add_argument("--certs", default="1,0", help="O3G_OPT_CERT values to compare (2 = forced)")
 a = ap.parse_args()
 
 import numpy as np  # noqa: E402
@@ -40,7 +41,8 @@ ctx.set_target(tgt, nrm, w["dmax"])
 ctx.set_source(src, w["init_T"])
 n = len(src)
 out = {}
-for cert in (1, 0):
+certs = [int(x) for x in a.certs.split(",")]
+for cert in certs:
     ctx.set_option(o3g.OPT_CERT, cert)
     ctx.set_option(o3g.OPT_TIMING, 1)
     for _ in range(2):
@@ -55,4 +57,4 @@ for cert in (1, 0):
                       "k3_ms_per_pass": round(k3_ms / k3_n, 4)}), flush=True)
 for k in range(r.passes):
     print(k, *(f"{out[c]['fitness'][k]:.4f} srch={out[c]['searched_frac'][k]:.3f} cert={out[c]['cert_frac'][k]:.3f} cand={out[c]['cand_per_search'][k]:.1f}"
-               for c in (1, 0)))
+               for c in certs))

@@ -18,6 +18,7 @@ ap.add_argument("--bps", type=int, default=0)
 ap.add_argument("--coop-min", type=int, default=None)
 ap.add_argument("--prune-min", type=int, default=None)
 ap.add_argument("--interleave", type=int, default=None)
+ap.add_argument("--cert", type=int, default=None, help="O3G_OPT_CERT")
 ap.add_argument("--regime", default="init", choices=["init", "converged"])
 a = ap.parse_args()
 
@@ -44,6 +45,8 @@ if a.coop_min is not None:
     ctx.set_option(6, a.coop_min)
 if a.prune_min is not None:
     ctx.set_option(10, a.prune_min)
+if a.cert is not None:
+    ctx.set_option(13, a.cert)
 if a.interleave is not None:
     ctx.set_option(11, a.interleave)
 for _ in range(a.reps):

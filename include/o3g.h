@@ -300,6 +300,9 @@ o3g_status o3g_loopback_run(o3g_ctx* const* ctxs, int world, const double init_T
  *   of >= 2^20 queries), 1 = on, 0 = off (the previous winner then only
  *   bounds the next search, the warm start), 2 = on from the second pass
  *   regardless of fitness (experiments).
+ * O3G_OPT_CERT_SWEEP: how a certificate pass settles the certified queries:
+ *   0 = inside the search kernel's pre-pass (fused; default), 1 = a separate
+ *   streaming sweep kernel that flags the rest for the search (experiments).
  * O3G_OPT_TRACE_PASS: k >= 0 = o3g_icp_run also writes the correspondences
  *   of pass k (original source order) for o3g_last_run_trace; -1 = off
  *   (default). A testing hook: it adds a scattered index write to pass k.
@@ -307,7 +310,8 @@ o3g_status o3g_loopback_run(o3g_ctx* const* ctxs, int world, const double init_T
 enum { O3G_OPT_SEARCH = 1, O3G_OPT_GRID = 2, O3G_OPT_TIMING = 3, O3G_OPT_BLOCKS_PER_SM = 4,
        O3G_OPT_NBR_MASK = 5, O3G_OPT_COOP_MIN = 6, O3G_OPT_ESTIMATION = 7,
        O3G_OPT_SOURCE_ORDER = 8, O3G_OPT_TARGET_SORT = 9, O3G_OPT_PRUNE_MIN = 10,
-       O3G_OPT_INTERLEAVE = 11, O3G_OPT_XSORT = 12, O3G_OPT_CERT = 13, O3G_OPT_TRACE_PASS = 14 };
+       O3G_OPT_INTERLEAVE = 11, O3G_OPT_XSORT = 12, O3G_OPT_CERT = 13, O3G_OPT_TRACE_PASS = 14,
+       O3G_OPT_CERT_SWEEP = 15 };
 o3g_status o3g_set_option(o3g_ctx* ctx, int option, int64_t value);
 
 /* Sum of the correspondence-kernel (K3) durations of the last o3g_icp_run

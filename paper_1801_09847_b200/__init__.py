@@ -5,4 +5,4 @@ from .o3g import (Context, O3GError, InvalidArgument, RegistrationResult,  # noq
                   FLAG_DEGENERATE, FLAG_NO_CORRESPONDENCES, NTERMS,
                   OPT_SEARCH, OPT_GRID, OPT_TIMING, OPT_BLOCKS_PER_SM, OPT_NBR_MASK, OPT_COOP_MIN,
                   OPT_ESTIMATION, OPT_SOURCE_ORDER, OPT_TARGET_SORT, OPT_PRUNE_MIN, OPT_INTERLEAVE,
-                  OPT_XSORT, OPT_CERT, OPT_TRACE_PASS)
+                  OPT_XSORT, OPT_CERT, OPT_TRACE_PASS, OPT_CERT_SWEEP)

@@ -440,6 +440,89 @@ __device__ __forceinline__ bool stencil_live(const K3Args& a, const GridDev& g, 
     return (__ldg(&a.nbr_bits[k >> 5]) >> (k & 31)) & 1u;
 }
 
+// a 32-byte certificate record, one 256-bit load
+__device__ __forceinline__ void ld_cert(const float4* c, float4& x, float4& y) {
+    asm volatile("ld.global.nc.L1::no_allocate.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=f"(x.x), "=f"(x.y), "=f"(x.z), "=f"(x.w), "=f"(y.x), "=f"(y.y), "=f"(y.z), "=f"(y.w)
+                 : "l"(c));
+}
+
+// One query of a certificate pass (the sweep, or the fused pre-pass of
+// k3_balanced<CERT>): a valid certificate settles it (win / x, y, z / q / n /
+// d2 = its record, or no correspondence); an expired one gets s', its cell and
+// the occupancy test: dead -> a fresh certificate, live -> returns true (the
+// query needs the full search).
+struct Settled {
+    int win = -1;
+    bool certified = false;
+    double x = 0.0, y = 0.0, z = 0.0, d2 = 0.0;
+    float4 q = make_float4(0.f, 0.f, 0.f, 0.f), n = make_float4(0.f, 0.f, 0.f, 0.f);
+};
+template <bool WRITE_CORR>
+__device__ __forceinline__ bool cert_settle(const K3Args& a, const GridDev& g, const double* sT,
+                                            const float4 (*sDT)[3], const float* sDC, int pass, int gpass, int i,
+                                            float4 p, float4 ca, float4 cb, float Lout, float dmax_hi, Settled& r) {
+    bool need = false;
+    int& cwin = r.win;
+    double &tx = r.x, &ty = r.y, &tz = r.z, &cd2 = r.d2;
+    float4 &cq = r.q, &cn = r.n;
+    {
+        const bool cv = cert_valid(__float_as_uint(ca.y), pass, gpass, p.x, p.y, p.z, sDT, sDC, a.h_rd);
+        const int cj = __float_as_int(ca.x);
+        if (!cv || cj >= 0) xform_rn(sT, p.x, p.y, p.z, tx, ty, tz);
+        if (cv) {
+            if (cj >= 0) {
+                const double dx = __dsub_rn(tx, (double)ca.z), dy = __dsub_rn(ty, (double)ca.w),
+                             dz = __dsub_rn(tz, (double)cb.x);
+                const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+                if (d2 <= a.r2) {
+                    cwin = cj, cd2 = d2;
+                    cq = make_float4(ca.z, ca.w, cb.x, 0.f);
+                    cn = make_float4(cb.y, cb.z, cb.w, 0.f);
+                }
+            }
+            if (WRITE_CORR) a.corr_out[__float_as_int(p.w)] = cwin >= 0 ? __float_as_int(__ldg(&a.tpos[cwin].w)) : -1;
+        } else {
+            const double tc[3] = {__dmul_rn(__dsub_rn(tx, g.ox), g.inv_h), __dmul_rn(__dsub_rn(ty, g.oy), g.inv_h),
+                                  __dmul_rn(__dsub_rn(tz, g.oz), g.inv_h)};
+            const int cx = min(max(__double2int_rd(tc[0]), -2), g.nx + 1);   // = cell_coord
+            const int cy = min(max(__double2int_rd(tc[1]), -2), g.ny + 1);
+            const int cz = min(max(__double2int_rd(tc[2]), -2), g.nz + 1);
+            bool live = true;
+            if (a.nbr_bits) {
+                if (!g.hashed) {
+                    live = false;
+                    if (cx >= -1 && cx <= g.nx && cy >= -1 && cy <= g.ny && cz >= -1 && cz <= g.nz) {
+                        const int kc = (min(max(cz, 0), g.nz - 1) * g.ny + min(max(cy, 0), g.ny - 1)) * g.nx +
+                                       min(max(cx, 0), g.nx - 1);
+                        live = (__ldg(&a.nbr_bits[kc >> 5]) >> (kc & 31)) & 1u;
+                    }
+                } else {
+                    live = stencil_live(a, g, cx, cy, cz);
+                }
+            }
+            if (!live) {
+                // empty 27-cell stencil: every target is beyond its outer faces, at
+                // >= h + (the smallest gap to the own cell's faces); 2h + that gap
+                // if the 5^3-cell neighbourhood is empty too (dense grid)
+                const int cc[3] = {cx, cy, cz};
+                float reach = __fadd_rd(Lout, min_face_gap_t(g, tc, cc));
+                if (a.nbr2_bits && cx >= 0 && cx < g.nx && cy >= 0 && cy < g.ny && cz >= 0 && cz < g.nz) {
+                    const int kc = (cz * g.ny + cy) * g.nx + cx;
+                    if (!((__ldg(&a.nbr2_bits[kc >> 5]) >> (kc & 31)) & 1u)) reach = __fadd_rd(reach, Lout);
+                }
+                a.cert[2 * (size_t)i] = make_float4(__int_as_float(-1),
+                                                    __uint_as_float(cert_pack(gpass, __fsub_rd(reach, dmax_hi), a.inv_h_rd)),
+                                                    0.f, 0.f);
+                if (WRITE_CORR) a.corr_out[__float_as_int(p.w)] = -1;
+            }
+            need = live;
+        }
+        r.certified = cv;
+    }
+    return need;
+}
+
 // CERT: the certificate-mode search of a run with certificates (after
 // k3_sweep: the flagged queries only; rows staged up to the certificate goal;
 // every search leaves a certificate). A run with certificates launches both
@@ -490,7 +573,8 @@ __global__ void __launch_bounds__(kK3Threads, 4) k3_balanced(const K3Args a) {
     // 0.36), 1.145 vs 1.039 ms converged; fragment (fitness 0.55) step 11.01
     // -> 10.64 ms with 0.5 instead of 0.7). Results are the same either way.
     // (with certificates the pre-pass also settles the certified queries: always on)
-    const bool use_queue = need != nullptr || (a.nbr_bits != nullptr && !(!a.eval_T && a.st->passes > 0 && a.st->fit > 0.5));
+    const bool use_queue = CERT || need != nullptr ||
+                           (a.nbr_bits != nullptr && !(!a.eval_T && a.st->passes > 0 && a.st->fit > 0.5));
     const bool warm = a.prev_j && !a.eval_T && a.st->passes > 0;
     const float Lout = __fmul_rd(a.h_rd, 1.0f - 1.1920928955078125e-07f);   // stencil reach >= h (§5.1 margins)
     const float dmax_hi = __double2float_ru(a.dmax * (1.0 + 9.094947017729282e-13));
@@ -512,7 +596,8 @@ __global__ void __launch_bounds__(kK3Threads, 4) k3_balanced(const K3Args a) {
         pf = pf_base + 8 * lane < a.n ? __ldg((const unsigned long long*)(need + pf_base + 8 * lane)) : 0ull;
     }
     int nsearch = 0, ncand = 0;   // this lane's full searches and their candidates (statistics)
-    __shared__ int s_stat[kK3Threads / 32][2];
+    int ncert = 0;                // (fused certificate pass) queries settled by a certificate
+    __shared__ int s_stat[kK3Threads / 32][3];
     for (;;) {
         int i;
         if (use_queue) {
@@ -557,6 +642,21 @@ __global__ void __launch_bounds__(kK3Threads, 4) k3_balanced(const K3Args a) {
             bool live = false;
             if (i0 < a.n && need) {
                 live = __ldg(&need[i0]) != 0;   // (k3_sweep settled every other query)
+            } else if (CERT) {
+                // fused certificate pass (no sweep launch): this batch's queries
+                // with a valid certificate are settled here and their records
+                // join the warp's contraction; expired ones take the occupancy
+                // test, and the live ones are queued for the search below
+                Settled r;
+                if (i0 < a.n) {
+                    const float4 p0 = __ldg(&a.src[i0]);
+                    float4 ca, cb;
+                    ld_cert(a.cert + 2 * (size_t)i0, ca, cb);
+                    live = cert_settle<WRITE_CORR>(a, g, sT, sDT, sDC, pass, gpass, i0, p0, ca, cb, Lout, dmax_hi, r);
+                    ncert += r.certified ? 1 : 0;
+                    if (a.prev_j && !live && !r.certified) a.prev_j[i0] = -1;
+                }
+                accumulate_records(a, vw, lane, r.win, r.x, r.y, r.z, r.q, r.n, r.d2, acc0, acc1);
             } else if (i0 < a.n) {
                 const float4 p0 = __ldg(&a.src[i0]);
                 double tx, ty, tz;
@@ -1115,8 +1215,9 @@ __global__ void __launch_bounds__(kK3Threads, 4) k3_balanced(const K3Args a) {
     for (int o = 16; o; o >>= 1) {
         nsearch += __shfl_xor_sync(0xffffffffu, nsearch, o);
         ncand += __shfl_xor_sync(0xffffffffu, ncand, o);
+        ncert += __shfl_xor_sync(0xffffffffu, ncert, o);
     }
-    if (lane == 0) s_stat[warp][0] = nsearch, s_stat[warp][1] = ncand;
+    if (lane == 0) s_stat[warp][0] = nsearch, s_stat[warp][1] = ncand, s_stat[warp][2] = ncert;
     vw[(lane >> 2) * 8 + 2 * (lane & 3)] = acc0;   // C of this warp, on its own staging bytes
     vw[(lane >> 2) * 8 + 2 * (lane & 3) + 1] = acc1;
     __syncthreads();
@@ -1127,7 +1228,7 @@ __global__ void __launch_bounds__(kK3Threads, 4) k3_balanced(const K3Args a) {
         if (ci >= 0)
             for (int w = 0; w < kK3Threads / 32; ++w)
                 s += ((const double*)(k3smem + (size_t)w * k3v2_warp_bytes(g.hashed)))[ci];
-        if (threadIdx.x == kStatSearched || threadIdx.x == kStatCandidates)
+        if (threadIdx.x == kStatSearched || threadIdx.x == kStatCandidates || (CERT && threadIdx.x == kStatCertified))
             for (int w = 0; w < kK3Threads / 32; ++w) s += (double)s_stat[w][threadIdx.x - kStatSearched];
         a.block_partials[((size_t)blockIdx.y * gridDim.x + a.part_off + blockIdx.x) * kTermStride + threadIdx.x] = s;
     }
@@ -1187,79 +1288,16 @@ __global__ void __launch_bounds__(kK3Threads, 4) k3_balanced(const K3Args a) {
 // block.
 constexpr int kSweepThreads = 256;
 
-__device__ __forceinline__ void ld_cert(const float4* c, float4& x, float4& y) {
-    asm volatile("ld.global.nc.L1::no_allocate.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                 : "=f"(x.x), "=f"(x.y), "=f"(x.z), "=f"(x.w), "=f"(y.x), "=f"(y.y), "=f"(y.z), "=f"(y.w)
-                 : "l"(c));
-}
 
 template <bool WRITE_CORR>
 __device__ __forceinline__ int sweep_query(const K3Args& a, const GridDev& g, const double* sT,
                                             const float4 (*sDT)[3], const float* sDC, int pass, int gpass, int i, float4 p,
                                             float4 ca, float4 cb, float Lout, float dmax_hi,
                                             double (&acc)[kTerms]) {
-    int cwin = -1;
-    bool certified = false;
-    double tx = 0.0, ty = 0.0, tz = 0.0, cd2 = 0.0;
-    float4 cq = make_float4(0.f, 0.f, 0.f, 0.f), cn = cq;
-    if (i < a.n) {
-        const bool cv = cert_valid(__float_as_uint(ca.y), pass, gpass, p.x, p.y, p.z, sDT, sDC, a.h_rd);
-        const int cj = __float_as_int(ca.x);
-        bool need = false;
-        if (!cv || cj >= 0) xform_rn(sT, p.x, p.y, p.z, tx, ty, tz);
-        if (cv) {
-            if (cj >= 0) {
-                const double dx = __dsub_rn(tx, (double)ca.z), dy = __dsub_rn(ty, (double)ca.w),
-                             dz = __dsub_rn(tz, (double)cb.x);
-                const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
-                if (d2 <= a.r2) {
-                    cwin = cj, cd2 = d2;
-                    cq = make_float4(ca.z, ca.w, cb.x, 0.f);
-                    cn = make_float4(cb.y, cb.z, cb.w, 0.f);
-                }
-            }
-            if (WRITE_CORR) a.corr_out[__float_as_int(p.w)] = cwin >= 0 ? __float_as_int(__ldg(&a.tpos[cwin].w)) : -1;
-        } else {
-            const double tc[3] = {__dmul_rn(__dsub_rn(tx, g.ox), g.inv_h), __dmul_rn(__dsub_rn(ty, g.oy), g.inv_h),
-                                  __dmul_rn(__dsub_rn(tz, g.oz), g.inv_h)};
-            const int cx = min(max(__double2int_rd(tc[0]), -2), g.nx + 1);   // = cell_coord
-            const int cy = min(max(__double2int_rd(tc[1]), -2), g.ny + 1);
-            const int cz = min(max(__double2int_rd(tc[2]), -2), g.nz + 1);
-            bool live = true;
-            if (a.nbr_bits) {
-                if (!g.hashed) {
-                    live = false;
-                    if (cx >= -1 && cx <= g.nx && cy >= -1 && cy <= g.ny && cz >= -1 && cz <= g.nz) {
-                        const int kc = (min(max(cz, 0), g.nz - 1) * g.ny + min(max(cy, 0), g.ny - 1)) * g.nx +
-                                       min(max(cx, 0), g.nx - 1);
-                        live = (__ldg(&a.nbr_bits[kc >> 5]) >> (kc & 31)) & 1u;
-                    }
-                } else {
-                    live = stencil_live(a, g, cx, cy, cz);
-                }
-            }
-            if (!live) {
-                // empty 27-cell stencil: every target is beyond its outer faces, at
-                // >= h + (the smallest gap to the own cell's faces); 2h + that gap
-                // if the 5^3-cell neighbourhood is empty too (dense grid)
-                const int cc[3] = {cx, cy, cz};
-                float reach = __fadd_rd(Lout, min_face_gap_t(g, tc, cc));
-                if (a.nbr2_bits && cx >= 0 && cx < g.nx && cy >= 0 && cy < g.ny && cz >= 0 && cz < g.nz) {
-                    const int kc = (cz * g.ny + cy) * g.nx + cx;
-                    if (!((__ldg(&a.nbr2_bits[kc >> 5]) >> (kc & 31)) & 1u)) reach = __fadd_rd(reach, Lout);
-                }
-                a.cert[2 * (size_t)i] = make_float4(__int_as_float(-1),
-                                                    __uint_as_float(cert_pack(gpass, __fsub_rd(reach, dmax_hi), a.inv_h_rd)),
-                                                    0.f, 0.f);
-                if (WRITE_CORR) a.corr_out[__float_as_int(p.w)] = -1;
-            }
-            need = live;
-        }
-        a.need[i] = need ? 1 : 0;
-        certified = cv;
-    }
-    if (cwin >= 0) acc_record(a, acc, tx, ty, tz, cq, cn, cd2);
-    return certified ? 1 : 0;
+    Settled r;
+    if (i < a.n) a.need[i] = cert_settle<WRITE_CORR>(a, g, sT, sDT, sDC, pass, gpass, i, p, ca, cb, Lout, dmax_hi, r) ? 1 : 0;
+    if (r.win >= 0) acc_record(a, acc, r.x, r.y, r.z, r.q, r.n, r.d2);
+    return r.certified ? 1 : 0;
 }
 
 // TMA rings of the sweep: each warp owns kSweepStages stages of one batch (32

@@ -135,6 +135,7 @@ struct o3g_ctx {
     int prune_min = -1;   // variant 1 row pruning: -1 auto, -2 never, >= 0 threshold
     int interleave = -1;  // variant 1 batch interleave: -1 auto, 0 off, 1 on
     int xsort = -1;       // target x-order inside cells: -1 auto, 0 off, 1 on
+    int cert_sweep = 0;   // certificate passes: 0 fused into the search kernel, 1 separate sweep kernel
     int cert_opt = -1;    // correspondence certificates in the run loop: -1 auto, 0 off, 1 on (§5.5)
     int trace_pass = -1;  // o3g_icp_run: record the correspondences of this pass
     // certificate goal: searches stage rows up to the previous
@@ -403,6 +404,10 @@ o3g_status o3g_set_option(o3g_ctx* c, int option, int64_t value) {
         case O3G_OPT_CERT:
             if (value < -1 || value > 2) return fail(O3G_ERR_INVALID_ARGUMENT, "cert must be -1, 0, 1 or 2");
             c->cert_opt = (int)value;
+            break;
+        case O3G_OPT_CERT_SWEEP:
+            if (value < 0 || value > 1) return fail(O3G_ERR_INVALID_ARGUMENT, "cert sweep must be 0 or 1");
+            c->cert_sweep = (int)value;
             break;
         case O3G_OPT_TRACE_PASS:
             if (value < -1 || value > 100000) return fail(O3G_ERR_INVALID_ARGUMENT, "trace pass must be in [-1, 100000]");
@@ -836,7 +841,7 @@ static o3g_status enqueue_pass(o3g_ctx* c, int blocks, bool write_corr, int32_t*
         ka.cert = cert;
         ka.pass_expect = pass;
         ka.part_total = blocks;
-        if (cert && sblocks > 0) {
+        if (cert && sblocks > 0 && c->cert_sweep) {
             ka.need = c->need.as<uint8_t>();
             launch_k3_sweep(ka, sblocks, write_corr, c->exec);
             ++*nlaunch;
@@ -856,7 +861,7 @@ static o3g_status enqueue_pass(o3g_ctx* c, int blocks, bool write_corr, int32_t*
         *nlaunch += (ka.cert && k3_variant(c) == 1) ? 2 : 1;   // (both search instantiations)
     }
     if (ev1) CK(cudaEventRecordWithFlags(ev1, c->exec, cudaEventRecordExternal));
-    const int nb = c->n_local > 0 ? blocks + (cert ? sblocks : 0) : 0;
+    const int nb = c->n_local > 0 ? blocks + (cert && c->cert_sweep ? sblocks : 0) : 0;
     double* gat = c->gathered.as<double>();
     IcpState* st = c->state.as<IcpState>();
     if (fused) {

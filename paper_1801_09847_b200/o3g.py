@@ -28,7 +28,7 @@ FLAG_DEGENERATE = 2
 NTERMS = 29
 (OPT_SEARCH, OPT_GRID, OPT_TIMING, OPT_BLOCKS_PER_SM, OPT_NBR_MASK, OPT_COOP_MIN, OPT_ESTIMATION,
  OPT_SOURCE_ORDER, OPT_TARGET_SORT, OPT_PRUNE_MIN, OPT_INTERLEAVE, OPT_XSORT, OPT_CERT,
- OPT_TRACE_PASS) = range(1, 15)
+ OPT_TRACE_PASS, OPT_CERT_SWEEP) = range(1, 16)
 
 
 class O3GError(RuntimeError):

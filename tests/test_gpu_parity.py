@@ -295,11 +295,11 @@ def test_invalid_arguments(o3g, workloads):
     # option ranges (include/o3g.h): every invalid value is rejected, valid ones accepted
     with o3g.Context(0) as ctx:
         for opt, bad_v in ((1, 5), (1, -1), (2, 3), (4, 65), (6, -2), (7, 2), (8, 2), (9, 2), (10, -4),
-                           (11, 2), (11, -2), (12, 2), (13, 3), (13, -2), (14, -2), (99, 0)):
+                           (11, 2), (11, -2), (12, 2), (13, 3), (13, -2), (14, -2), (15, 2), (15, -1), (99, 0)):
             with pytest.raises(E):
                 ctx.set_option(opt, bad_v)
         for opt, ok_v in ((1, 4), (2, 0), (3, 1), (4, 0), (5, 0), (6, -1), (7, 0), (8, 1), (9, 0), (10, -2),
-                          (11, -1), (12, -1), (13, -1), (13, 2), (14, 3), (14, -1)):
+                          (11, -1), (12, -1), (13, -1), (13, 2), (14, 3), (14, -1), (15, 1), (15, 0)):
             ctx.set_option(opt, ok_v)
 
 
@@ -565,8 +565,8 @@ def _trace_cases(workloads):
 
 
 @pytest.mark.parametrize("grid", list(GRID))
-@pytest.mark.parametrize("cert", [1, 0])
-def test_run_loop_every_pass(o3g, workloads, grid, cert):
+@pytest.mark.parametrize("cert,sweep", [(1, 0), (0, 0), (1, 1), (2, 0)])
+def test_run_loop_every_pass(o3g, workloads, grid, cert, sweep):
     """The run loop's own passes — warm-started searches and, with
     O3G_OPT_CERT, queries settled by a correspondence certificate (DESIGN.md
     §5.5) — are only reachable inside o3g_icp_run. o3g_last_run_trace gives
@@ -574,13 +574,16 @@ def test_run_loop_every_pass(o3g, workloads, grid, cert):
     the oracle's pass at that T (R14; count exact), and at traced passes the
     correspondences must be bit-identical. With certificates on, fewer
     queries run the full search than with them off, and the loop's T is
-    bitwise the same either way."""
+    bitwise the same either way. Certificate passes run fused into the
+    search kernel (sweep 0) or with the separate sweep kernel (sweep 1);
+    cert 2 forces them from the second pass (the T_init regime)."""
     for name, w, T0, iters, _ in _trace_cases(workloads):
         T0 = w["init_T"] if T0 is None else T0
         n = len(w["source"])
         grid_o = oracle.Grid(w["target"], w["dmax"])
         with _ctx(o3g, w, "balanced", grid, order_T=T0) as ctx:
             ctx.set_option(o3g.OPT_CERT, cert)
+            ctx.set_option(o3g.OPT_CERT_SWEEP, sweep)
             r = ctx.run(T0, iters, 0.0, 0.0)
             tr = ctx.last_run_trace(r.passes)
             refs = [oracle.step(T, w["source"], w["target"], w["target_normals"], w["dmax"], grid=grid_o)
@@ -599,7 +602,7 @@ def test_run_loop_every_pass(o3g, workloads, grid, cert):
                 assert np.array_equal(got, refs[k]["corr"]), (name, grid, cert, k, int((got != refs[k]["corr"]).sum()))
             ctx.set_option(o3g.OPT_TRACE_PASS, -1)
             # the other setting: same loop, bit for bit (certificates are exact)
-            ctx.set_option(o3g.OPT_CERT, 1 - cert)
+            ctx.set_option(o3g.OPT_CERT, 0 if cert else 1)
             r3 = ctx.run(T0, iters, 0.0, 0.0)
             t3 = ctx.last_run_trace(r3.passes)
         assert r3.passes == r.passes
@@ -609,6 +612,8 @@ def test_run_loop_every_pass(o3g, workloads, grid, cert):
         assert on["searched"][0] == off["searched"][0]
         # (a pass runs with certificates once the previous pass matched > 1/2 of
         # the source; before that, both settings run the same plain pass)
+        if cert == 2 and r.passes > 2:
+            assert on["certified"][2:].sum() > 0, name
         if on["certified"].sum() > 0:
             assert on["searched"][1:].sum() < off["searched"][1:].sum(), name
         else:

@@ -161,6 +161,28 @@ __global__ void k_cs_fill(const uint32_t* __restrict__ keys, int64_t n, int64_t 
     }
 }
 
+// Source shard by key range (world > 1): a histogram of the top bits of the
+// ordering keys (shared-memory privatised, 2^12 buckets), then the stable
+// selection of the keys in a bucket range; sorting only the selection gives
+// exactly the slice of the full stable sort (ties keep original-index order).
+__global__ void k_key_hist(const uint32_t* __restrict__ keys, int64_t n, int shift, uint32_t* __restrict__ hist) {
+    __shared__ uint32_t h[kShardBuckets];
+    for (int t = threadIdx.x; t < kShardBuckets; t += blockDim.x) h[t] = 0u;
+    __syncthreads();
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        atomicAdd(&h[min(keys[i] >> shift, (uint32_t)kShardBuckets - 1u)], 1u);
+    __syncthreads();
+    for (int t = threadIdx.x; t < kShardBuckets; t += blockDim.x)
+        if (h[t]) atomicAdd(&hist[t], h[t]);
+}
+__global__ void k_key_flags(const uint32_t* __restrict__ keys, int64_t n, int shift, uint32_t blo, uint32_t bhi,
+                            uint8_t* __restrict__ flags) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t b = min(keys[i] >> shift, (uint32_t)kShardBuckets - 1u);
+        flags[i] = (b >= blo && b <= bhi) ? 1 : 0;
+    }
+}
+
 // hashed grid: occupancy of coarse cells (2^shift fine cells per axis), the
 // live-query test's structure when no dense per-cell bitmap fits
 __global__ void k_coarse_bits(const float4* __restrict__ tpos, int64_t n, GridDev g, int shift, int cnx, int cny,
@@ -339,6 +361,14 @@ void launch_cs_runs(const uint32_t* keys, int64_t n, int32_t* runs, uint32_t* oc
 void launch_cs_fill(const uint32_t* keys, int64_t n, int64_t cells, int32_t* cs, uint32_t* occ_bits,
                     cudaStream_t s) {
     k_cs_fill<<<blocks_for(n / 32 + 1, 8), 256, 0, s>>>(keys, n, cells, cs, occ_bits);
+}
+void launch_key_hist(const uint32_t* keys, int64_t n, int shift, uint32_t* hist, int sms, cudaStream_t s) {
+    cudaMemsetAsync(hist, 0, kShardBuckets * sizeof(uint32_t), s);
+    k_key_hist<<<blocks_for(n, 256, sms * 2), 256, 0, s>>>(keys, n, shift, hist);
+}
+void launch_key_flags(const uint32_t* keys, int64_t n, int shift, uint32_t blo, uint32_t bhi, uint8_t* flags,
+                      cudaStream_t s) {
+    k_key_flags<<<blocks_for(n, 256), 256, 0, s>>>(keys, n, shift, blo, bhi, flags);
 }
 void launch_coarse_bits(const float4* tpos, int64_t n, const GridDev& g, int shift, int cnx, int cny,
                         uint32_t* bits, cudaStream_t s) {

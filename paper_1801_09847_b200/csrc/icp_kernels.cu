@@ -447,6 +447,13 @@ __device__ __forceinline__ void ld_cert(const float4* c, float4& x, float4& y) {
                  : "l"(c));
 }
 
+// (the fused pre-pass: the record was prefetched into L1 one batch ahead)
+__device__ __forceinline__ void ld_cert_l1(const float4* c, float4& x, float4& y) {
+    asm volatile("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=f"(x.x), "=f"(x.y), "=f"(x.z), "=f"(x.w), "=f"(y.x), "=f"(y.y), "=f"(y.z), "=f"(y.w)
+                 : "l"(c));
+}
+
 // One query of a certificate pass (the sweep, or the fused pre-pass of
 // k3_balanced<CERT>): a valid certificate settles it (win / x, y, z / q / n /
 // d2 = its record, or no correspondence); an expired one gets s', its cell and
@@ -637,8 +644,12 @@ __global__ void __launch_bounds__(kK3Threads, 4) k3_balanced(const K3Args a) {
             // source (LiDAR points next to the sensor) spread over all warps
             const int i0 = a.ilv ? min(lane * a.ilv + (base >> 5), a.n) : base + lane;
             base += nw * 32;
-            // the warp's next source batch: in flight while this one is processed
-            if (!a.ilv && !need && base + lane < a.n) asm volatile("prefetch.global.L1 [%0];" ::"l"(a.src + base + lane));
+            // the warp's next source batch (and, fused certificate pass, its
+            // certificates): in flight while this one is processed
+            if (!a.ilv && !need && base + lane < a.n) {
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(a.src + base + lane));
+                if (CERT) asm volatile("prefetch.global.L1 [%0];" ::"l"(a.cert + 2 * (size_t)(base + lane)));
+            }
             bool live = false;
             if (i0 < a.n && need) {
                 live = __ldg(&need[i0]) != 0;   // (k3_sweep settled every other query)
@@ -651,7 +662,7 @@ __global__ void __launch_bounds__(kK3Threads, 4) k3_balanced(const K3Args a) {
                 if (i0 < a.n) {
                     const float4 p0 = __ldg(&a.src[i0]);
                     float4 ca, cb;
-                    ld_cert(a.cert + 2 * (size_t)i0, ca, cb);
+                    ld_cert_l1(a.cert + 2 * (size_t)i0, ca, cb);
                     live = cert_settle<WRITE_CORR>(a, g, sT, sDT, sDC, pass, gpass, i0, p0, ca, cb, Lout, dmax_hi, r);
                     ncert += r.certified ? 1 : 0;
                     if (a.prev_j && !live && !r.certified) a.prev_j[i0] = -1;

@@ -154,7 +154,7 @@ struct o3g_ctx {
     bool nbr_ready = false;
     int cshift = 0, cnx = 0, cny = 0;   // hashed grid: coarse occupancy bitmap (nbr_a)
     // scratch
-    DevBuf keys_a, keys_b, vals_a, vals_b, cub_tmp, stage_a, stage_b, stage_c, misc;
+    DevBuf keys_a, keys_b, vals_a, vals_b, cub_tmp, stage_a, stage_b, stage_c, misc, misc2;
     // voxel_down_sample / multi-scale scratch
     DevBuf vk_a, vk_b, vflags, vrunid, vstarts, ms_src, ms_tgt, ms_nrm;
     DevBuf ms_in_src, ms_in_tgt, ms_in_nrm;   // multi-scale: host inputs copied once
@@ -344,7 +344,7 @@ o3g_status o3g_destroy(o3g_ctx* c) {
     invalidate_graph(c);
     for (auto ev : c->events) cudaEventDestroy(ev);
     DevBuf* bufs[] = {&c->tpos, &c->tnrm, &c->cell_start, &c->counts, &c->nbr_a, &c->nbr_b, &c->keys_a, &c->keys_b,
-                      &c->vals_a, &c->vals_b, &c->cub_tmp, &c->stage_a, &c->stage_b, &c->stage_c, &c->misc,
+                      &c->vals_a, &c->vals_b, &c->cub_tmp, &c->stage_a, &c->stage_b, &c->stage_c, &c->misc, &c->misc2,
                       &c->src4, &c->partials, &c->gathered, &c->state, &c->hist_fit, &c->hist_rmse,
                       &c->vk_a, &c->vk_b, &c->vflags, &c->vrunid, &c->vstarts, &c->ms_src,
                       &c->ms_tgt, &c->ms_nrm, &c->ev_T, &c->ev_part, &c->ev_out, &c->tiles, &c->tflag, &c->prevj, &c->ms_in_src, &c->ms_in_tgt, &c->ms_in_nrm, &c->xk_a, &c->xk_b, &c->xpos, &c->xnrm, &c->cert, &c->hist_T, &c->hist_terms, &c->trace_corr, &c->nbr_c, &c->need};
@@ -665,10 +665,53 @@ o3g_status o3g_set_source(o3g_ctx* c, const float* xyz, int64_t n, const double 
     }
     launch_cell_keys(dx, n, c->g, order_T ? T12 : nullptr, c->keys_a.as<uint32_t>(),
                      c->vals_a.as<int32_t>(), c->exec, brick);
-    TRY(sort_pairs(c, n, brick ? 32 : bits_for((uint64_t)(c->g.table_size - 1))));
+    const int kbits = brick ? 32 : bits_for((uint64_t)(c->g.table_size - 1));
     const int64_t lo = (int64_t)c->rank * n / c->world, hi = (int64_t)(c->rank + 1) * n / c->world;
+    int64_t base = 0;   // sorted position of the first sorted (selected) key
+    if (c->world > 1 && !brick && c->search != 4 && hi > lo) {
+        // this rank's slice [lo, hi) of the stable key order without sorting
+        // all n: histogram of the top key bits, the bucket range holding the
+        // slice, a stable selection of those keys (original-index order),
+        // then a sort of the selection only (no replicated
+        // full-source sort per rank)
+        const int shift = kbits > 12 ? kbits - 12 : 0;
+        TRY(c->misc2.ensure(kShardBuckets * sizeof(uint32_t)));
+        launch_key_hist(c->keys_a.as<uint32_t>(), n, shift, c->misc2.as<uint32_t>(), c->sms, c->exec);
+        std::vector<uint32_t> hist(kShardBuckets);
+        CK(cudaMemcpyAsync(hist.data(), c->misc2.p, kShardBuckets * sizeof(uint32_t), cudaMemcpyDeviceToHost, c->exec));
+        CK(cudaStreamSynchronize(c->exec));
+        int64_t cum = 0;
+        int blo = -1, bhi = -1;
+        for (int b = 0; b < kShardBuckets; ++b) {
+            const int64_t nx = cum + hist[b];
+            if (blo < 0 && nx > lo) blo = b, base = cum;
+            if (nx >= hi) { bhi = b; break; }
+            cum = nx;
+        }
+        int64_t nsel = 0;
+        for (int b = blo; b <= bhi; ++b) nsel += hist[b];
+        TRY(c->tflag.ensure((size_t)n + 64));
+        launch_key_flags(c->keys_a.as<uint32_t>(), n, shift, (uint32_t)blo, (uint32_t)bhi, c->tflag.as<uint8_t>(),
+                         c->exec);
+        TRY(c->misc.ensure(128));
+        int32_t* d_nsel = (int32_t*)(c->misc.as<uint32_t>() + 20);
+        size_t tmp = 0;
+        CK(cub::DeviceSelect::Flagged(nullptr, tmp, c->keys_a.as<uint32_t>(), c->tflag.as<uint8_t>(),
+                                      c->keys_b.as<uint32_t>(), d_nsel, (int)n, c->exec));
+        TRY(c->cub_tmp.ensure(tmp));
+        CK(cub::DeviceSelect::Flagged(c->cub_tmp.p, tmp, c->keys_a.as<uint32_t>(), c->tflag.as<uint8_t>(),
+                                      c->keys_b.as<uint32_t>(), d_nsel, (int)n, c->exec));
+        CK(cub::DeviceSelect::Flagged(c->cub_tmp.p, tmp, c->vals_a.as<int32_t>(), c->tflag.as<uint8_t>(),
+                                      c->vals_b.as<int32_t>(), d_nsel, (int)n, c->exec));
+        CK(cudaMemcpyAsync(c->keys_a.p, c->keys_b.p, (size_t)nsel * 4, cudaMemcpyDeviceToDevice, c->exec));
+        CK(cudaMemcpyAsync(c->vals_a.p, c->vals_b.p, (size_t)nsel * 4, cudaMemcpyDeviceToDevice, c->exec));
+        TRY(sort_pairs(c, nsel, kbits));
+        c->launches += 7;
+    } else {
+        TRY(sort_pairs(c, n, kbits));
+    }
     TRY(c->src4.ensure((size_t)(hi - lo > 0 ? hi - lo : 1) * sizeof(float4)));
-    if (hi > lo) launch_gather_source(dx, c->vals_b.as<int32_t>(), lo, hi, c->src4.as<float4>(), c->exec);
+    if (hi > lo) launch_gather_source(dx, c->vals_b.as<int32_t>(), lo - base, hi - base, c->src4.as<float4>(), c->exec);
     c->launches += 3;
     c->ntiles = 0;
     if (c->search == 4 && !c->g.hashed && hi > lo) {
@@ -826,7 +869,12 @@ static o3g_status enqueue_pass(o3g_ctx* c, int blocks, bool write_corr, int32_t*
                                int phase = 0, int pass = -1) {
     const TailHist hist{c->hist_fit.as<double>(), c->hist_rmse.as<double>(), c->hist_T.as<double>(),
                         c->hist_terms.as<double>()};
-    if (ev0) CK(cudaEventRecordWithFlags(ev0, c->exec, cudaEventRecordExternal));
+    // (timing events: external event nodes inside the run graph's capture,
+    // plain records on the loopback's uncaptured stream)
+    cudaStreamCaptureStatus capst = cudaStreamCaptureStatusNone;
+    CK(cudaStreamIsCapturing(c->exec, &capst));
+    const unsigned evflags = capst == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : cudaEventRecordDefault;
+    if (ev0) CK(cudaEventRecordWithFlags(ev0, c->exec, evflags));
     const bool fused = c->world == 1 && k3_variant(c) == 1 && c->n_local > 0;
     if (c->estimation) tail_mode |= TAIL_P2P;
     if (phase == 2) {
@@ -860,7 +908,7 @@ static o3g_status enqueue_pass(o3g_ctx* c, int blocks, bool write_corr, int32_t*
         launch_k3(ka, blocks, k3_variant(c), write_corr, c->exec);
         *nlaunch += (ka.cert && k3_variant(c) == 1) ? 2 : 1;   // (both search instantiations)
     }
-    if (ev1) CK(cudaEventRecordWithFlags(ev1, c->exec, cudaEventRecordExternal));
+    if (ev1) CK(cudaEventRecordWithFlags(ev1, c->exec, evflags));
     const int nb = c->n_local > 0 ? blocks + (cert && c->cert_sweep ? sblocks : 0) : 0;
     double* gat = c->gathered.as<double>();
     IcpState* st = c->state.as<IcpState>();
@@ -1247,12 +1295,26 @@ o3g_status o3g_loopback_run(o3g_ctx* const* ctxs, int world, const double init_T
             TRY(run_prologue(c, certm[r], trace[r]));
         }
         int nl = 0;
+        // O3G_OPT_TIMING on a rank: its correspondence kernels are timed per
+        // pass (the ranks run one after another on this device, so each
+        // rank's time is its kernels' alone: the per-GPU phase times of a
+        // world-P run)
+        for (int r = 0; r < world; ++r) {
+            o3g_ctx* c = ctxs[r];
+            const size_t nev = c->timing ? 2 * (size_t)(max_iterations + 1) : 0;
+            while (c->events.size() < nev) {
+                cudaEvent_t ev;
+                CK(cudaEventCreate(&ev));
+                c->events.push_back(ev);
+            }
+        }
         for (int p = 0; p <= max_iterations; ++p) {
             for (int r = 0; r < world; ++r) {
                 o3g_ctx* c = ctxs[r];
                 const bool wc = trace[r] && p == c->trace_pass;
-                TRY(enqueue_pass(c, blocks[r], wc, wc ? c->trace_corr.as<int32_t>() : nullptr, TAIL_SOLVE, nullptr,
-                                 nullptr, &nl, c->prevj.as<int32_t>(), certm[r] ? c->cert.as<float4>() : nullptr,
+                TRY(enqueue_pass(c, blocks[r], wc, wc ? c->trace_corr.as<int32_t>() : nullptr, TAIL_SOLVE,
+                                 c->timing ? c->events[2 * p] : nullptr, c->timing ? c->events[2 * p + 1] : nullptr,
+                                 &nl, c->prevj.as<int32_t>(), certm[r] ? c->cert.as<float4>() : nullptr,
                                  certm[r] ? sblocks[r] : 0, world > 1 ? 1 : 0, p));
             }
             if (world == 1) continue;
@@ -1288,7 +1350,16 @@ o3g_status o3g_loopback_run(o3g_ctx* const* ctxs, int world, const double init_T
         c->last_passes = sr.passes;
         c->trace_valid = c->trace_pass >= 0 && c->trace_pass < sr.passes;
         c->last_k3_ms = 0.0;
+        c->last_tail_ms = 0.0;
         c->last_k3_launches = 0;
+        if (c->timing) {
+            for (int p = 0; p < sr.passes; ++p) {
+                float ms = 0.f;
+                CK(cudaEventElapsedTime(&ms, c->events[2 * p], c->events[2 * p + 1]));
+                c->last_k3_ms += ms;
+            }
+            c->last_k3_launches = sr.passes;
+        }
     }
     memcpy(T_out, s0.T, 16 * sizeof(double));
     *fitness = s0.fit;

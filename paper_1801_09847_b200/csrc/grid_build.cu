@@ -165,14 +165,22 @@ __global__ void k_cs_fill(const uint32_t* __restrict__ keys, int64_t n, int64_t 
 // ordering keys (shared-memory privatised, 2^12 buckets), then the stable
 // selection of the keys in a bucket range; sorting only the selection gives
 // exactly the slice of the full stable sort (ties keep original-index order).
-__global__ void k_key_hist(const uint32_t* __restrict__ keys, int64_t n, int shift, uint32_t* __restrict__ hist) {
-    __shared__ uint32_t h[kShardBuckets];
-    for (int t = threadIdx.x; t < kShardBuckets; t += blockDim.x) h[t] = 0u;
+__global__ void k_key_hist(const uint32_t* __restrict__ keys, int64_t n, int shift, const uint32_t* __restrict__ live,
+                           uint32_t* __restrict__ hist) {
+    // hist[b] = points of bucket b, hist[kShardBuckets + b] = those whose
+    // 27-cell stencil holds a target (dense grid: bit `key` of the dilated
+    // occupancy bitmap; the live ones run the full search: the work estimate)
+    __shared__ uint32_t h[2 * kShardBuckets];
+    for (int t = threadIdx.x; t < 2 * kShardBuckets; t += blockDim.x) h[t] = 0u;
     __syncthreads();
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-        atomicAdd(&h[min(keys[i] >> shift, (uint32_t)kShardBuckets - 1u)], 1u);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t k = keys[i];
+        const uint32_t b = min(k >> shift, (uint32_t)kShardBuckets - 1u);
+        atomicAdd(&h[b], 1u);
+        if (live && ((__ldg(&live[k >> 5]) >> (k & 31)) & 1u)) atomicAdd(&h[kShardBuckets + b], 1u);
+    }
     __syncthreads();
-    for (int t = threadIdx.x; t < kShardBuckets; t += blockDim.x)
+    for (int t = threadIdx.x; t < 2 * kShardBuckets; t += blockDim.x)
         if (h[t]) atomicAdd(&hist[t], h[t]);
 }
 __global__ void k_key_flags(const uint32_t* __restrict__ keys, int64_t n, int shift, uint32_t blo, uint32_t bhi,
@@ -362,9 +370,10 @@ void launch_cs_fill(const uint32_t* keys, int64_t n, int64_t cells, int32_t* cs,
                     cudaStream_t s) {
     k_cs_fill<<<blocks_for(n / 32 + 1, 8), 256, 0, s>>>(keys, n, cells, cs, occ_bits);
 }
-void launch_key_hist(const uint32_t* keys, int64_t n, int shift, uint32_t* hist, int sms, cudaStream_t s) {
-    cudaMemsetAsync(hist, 0, kShardBuckets * sizeof(uint32_t), s);
-    k_key_hist<<<blocks_for(n, 256, sms * 2), 256, 0, s>>>(keys, n, shift, hist);
+void launch_key_hist(const uint32_t* keys, int64_t n, int shift, const uint32_t* live, uint32_t* hist, int sms,
+                     cudaStream_t s) {
+    cudaMemsetAsync(hist, 0, 2 * kShardBuckets * sizeof(uint32_t), s);
+    k_key_hist<<<blocks_for(n, 256, sms * 2), 256, 0, s>>>(keys, n, shift, live, hist);
 }
 void launch_key_flags(const uint32_t* keys, int64_t n, int shift, uint32_t blo, uint32_t bhi, uint8_t* flags,
                       cudaStream_t s) {

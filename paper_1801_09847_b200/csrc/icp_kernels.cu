@@ -1280,6 +1280,11 @@ __global__ void __launch_bounds__(kK3Threads, 4) k3_balanced(const K3Args a) {
         terms[threadIdx.x] = s;
     }
     __syncthreads();
+    if (a.fuse_mode & TAIL_WRITE_RANK) {   // (distributed: this rank's slot; the exchange and the solve follow)
+        if (threadIdx.x < kTermStride) a.gathered[a.rank * kTermStride + threadIdx.x] = terms[threadIdx.x];
+        if (threadIdx.x == 0) *a.counter = 0u;
+        return;
+    }
     if (threadIdx.x == 0) {
         *a.counter = 0u;
         tail_finish(terms, a.st_rw, TailHist{a.hist_fit, a.hist_rmse, a.hist_T, a.hist_terms}, a.fuse_mode);

@@ -135,6 +135,7 @@ struct o3g_ctx {
     int prune_min = -1;   // variant 1 row pruning: -1 auto, -2 never, >= 0 threshold
     int interleave = -1;  // variant 1 batch interleave: -1 auto, 0 off, 1 on
     int xsort = -1;       // target x-order inside cells: -1 auto, 0 off, 1 on
+    double shard_live_weight = 8.0;   // multi-rank split: work of a live query / a dead one
     int cert_sweep = 0;   // certificate passes: 0 fused into the search kernel, 1 separate sweep kernel
     int cert_opt = -1;    // correspondence certificates in the run loop: -1 auto, 0 off, 1 on (§5.5)
     int trace_pass = -1;  // o3g_icp_run: record the correspondences of this pass
@@ -323,6 +324,7 @@ o3g_status o3g_create(o3g_ctx** out, int device, void* cuda_stream) {
     o3g_ctx* c = new o3g_ctx();
     c->device = device;
     c->sms = prop.multiProcessorCount;
+    if (const char* sw = getenv("O3G_SHARD_LIVE_WEIGHT")) c->shard_live_weight = atof(sw);
     if (const char* gs = getenv("O3G_CERT_GOAL")) sscanf(gs, "%lf,%lf", &c->rhog_mul, &c->rhog_cap);
     c->user = (cudaStream_t)cuda_stream;
     cudaError_t e = cudaStreamCreate(&c->exec);
@@ -666,47 +668,63 @@ o3g_status o3g_set_source(o3g_ctx* c, const float* xyz, int64_t n, const double 
     launch_cell_keys(dx, n, c->g, order_T ? T12 : nullptr, c->keys_a.as<uint32_t>(),
                      c->vals_a.as<int32_t>(), c->exec, brick);
     const int kbits = brick ? 32 : bits_for((uint64_t)(c->g.table_size - 1));
-    const int64_t lo = (int64_t)c->rank * n / c->world, hi = (int64_t)(c->rank + 1) * n / c->world;
+    int64_t lo = (int64_t)c->rank * n / c->world, hi = (int64_t)(c->rank + 1) * n / c->world;
     int64_t base = 0;   // sorted position of the first sorted (selected) key
-    if (c->world > 1 && !brick && c->search != 4 && hi > lo) {
-        // this rank's slice [lo, hi) of the stable key order without sorting
-        // all n: histogram of the top key bits, the bucket range holding the
-        // slice, a stable selection of those keys (original-index order),
-        // then a sort of the selection only (no replicated
-        // full-source sort per rank)
+    if (c->world > 1 && !brick && c->search != 4) {
+        // this rank's shard without sorting all n: a histogram
+        // of the top 12 key bits with, per bucket, the queries whose stencil
+        // holds a target at order_T (they run the full search); the ranks
+        // split the bucket sequence into contiguous ranges of equal estimated
+        // work (live 8, dead 1: equal counts left the densest slab's rank with
+        // 1.8x the mean work at 8 ranks), then select (stably) and sort only
+        // their own buckets. Every rank derives the same split.
         const int shift = kbits > 12 ? kbits - 12 : 0;
-        TRY(c->misc2.ensure(kShardBuckets * sizeof(uint32_t)));
-        launch_key_hist(c->keys_a.as<uint32_t>(), n, shift, c->misc2.as<uint32_t>(), c->sms, c->exec);
-        std::vector<uint32_t> hist(kShardBuckets);
-        CK(cudaMemcpyAsync(hist.data(), c->misc2.p, kShardBuckets * sizeof(uint32_t), cudaMemcpyDeviceToHost, c->exec));
+        TRY(c->misc2.ensure(2 * kShardBuckets * sizeof(uint32_t)));
+        const uint32_t* live = (!c->g.hashed && c->nbr_ready) ? c->nbr_a.as<uint32_t>() : nullptr;
+        launch_key_hist(c->keys_a.as<uint32_t>(), n, shift, live, c->misc2.as<uint32_t>(), c->sms, c->exec);
+        std::vector<uint32_t> hist(2 * kShardBuckets);
+        CK(cudaMemcpyAsync(hist.data(), c->misc2.p, hist.size() * sizeof(uint32_t), cudaMemcpyDeviceToHost, c->exec));
         CK(cudaStreamSynchronize(c->exec));
-        int64_t cum = 0;
-        int blo = -1, bhi = -1;
-        for (int b = 0; b < kShardBuckets; ++b) {
-            const int64_t nx = cum + hist[b];
-            if (blo < 0 && nx > lo) blo = b, base = cum;
-            if (nx >= hi) { bhi = b; break; }
-            cum = nx;
-        }
-        int64_t nsel = 0;
+        const double wl = c->shard_live_weight - 1.0;
+        double wtot = 0.0;
+        for (int b = 0; b < kShardBuckets; ++b) wtot += (double)hist[b] + wl * (double)hist[kShardBuckets + b];
+        // rank r owns buckets [B_r, B_(r+1)): B_r = first bucket whose preceding
+        // weight reaches r/world of the total
+        auto first_bucket = [&](int r) {
+            if (r <= 0) return 0;
+            if (r >= c->world) return kShardBuckets;
+            const double goal = wtot * (double)r / (double)c->world;
+            double cw = 0.0;
+            for (int b = 0; b < kShardBuckets; ++b) {
+                if (cw >= goal) return b;
+                cw += (double)hist[b] + wl * (double)hist[kShardBuckets + b];
+            }
+            return kShardBuckets;
+        };
+        const int blo = first_bucket(c->rank), bhi = first_bucket(c->rank + 1) - 1;
+        int64_t before = 0, nsel = 0;
+        for (int b = 0; b < blo; ++b) before += hist[b];
         for (int b = blo; b <= bhi; ++b) nsel += hist[b];
-        TRY(c->tflag.ensure((size_t)n + 64));
-        launch_key_flags(c->keys_a.as<uint32_t>(), n, shift, (uint32_t)blo, (uint32_t)bhi, c->tflag.as<uint8_t>(),
-                         c->exec);
-        TRY(c->misc.ensure(128));
-        int32_t* d_nsel = (int32_t*)(c->misc.as<uint32_t>() + 20);
-        size_t tmp = 0;
-        CK(cub::DeviceSelect::Flagged(nullptr, tmp, c->keys_a.as<uint32_t>(), c->tflag.as<uint8_t>(),
-                                      c->keys_b.as<uint32_t>(), d_nsel, (int)n, c->exec));
-        TRY(c->cub_tmp.ensure(tmp));
-        CK(cub::DeviceSelect::Flagged(c->cub_tmp.p, tmp, c->keys_a.as<uint32_t>(), c->tflag.as<uint8_t>(),
-                                      c->keys_b.as<uint32_t>(), d_nsel, (int)n, c->exec));
-        CK(cub::DeviceSelect::Flagged(c->cub_tmp.p, tmp, c->vals_a.as<int32_t>(), c->tflag.as<uint8_t>(),
-                                      c->vals_b.as<int32_t>(), d_nsel, (int)n, c->exec));
-        CK(cudaMemcpyAsync(c->keys_a.p, c->keys_b.p, (size_t)nsel * 4, cudaMemcpyDeviceToDevice, c->exec));
-        CK(cudaMemcpyAsync(c->vals_a.p, c->vals_b.p, (size_t)nsel * 4, cudaMemcpyDeviceToDevice, c->exec));
-        TRY(sort_pairs(c, nsel, kbits));
-        c->launches += 7;
+        lo = before, hi = before + nsel, base = before;
+        if (nsel > 0) {
+            TRY(c->tflag.ensure((size_t)n + 64));
+            launch_key_flags(c->keys_a.as<uint32_t>(), n, shift, (uint32_t)blo, (uint32_t)bhi,
+                             c->tflag.as<uint8_t>(), c->exec);
+            TRY(c->misc.ensure(128));
+            int32_t* d_nsel = (int32_t*)(c->misc.as<uint32_t>() + 20);
+            size_t tmp = 0;
+            CK(cub::DeviceSelect::Flagged(nullptr, tmp, c->keys_a.as<uint32_t>(), c->tflag.as<uint8_t>(),
+                                          c->keys_b.as<uint32_t>(), d_nsel, (int)n, c->exec));
+            TRY(c->cub_tmp.ensure(tmp));
+            CK(cub::DeviceSelect::Flagged(c->cub_tmp.p, tmp, c->keys_a.as<uint32_t>(), c->tflag.as<uint8_t>(),
+                                          c->keys_b.as<uint32_t>(), d_nsel, (int)n, c->exec));
+            CK(cub::DeviceSelect::Flagged(c->cub_tmp.p, tmp, c->vals_a.as<int32_t>(), c->tflag.as<uint8_t>(),
+                                          c->vals_b.as<int32_t>(), d_nsel, (int)n, c->exec));
+            CK(cudaMemcpyAsync(c->keys_a.p, c->keys_b.p, (size_t)nsel * 4, cudaMemcpyDeviceToDevice, c->exec));
+            CK(cudaMemcpyAsync(c->vals_a.p, c->vals_b.p, (size_t)nsel * 4, cudaMemcpyDeviceToDevice, c->exec));
+            TRY(sort_pairs(c, nsel, kbits));
+            c->launches += 7;
+        }
     } else {
         TRY(sort_pairs(c, n, kbits));
     }
@@ -875,7 +893,9 @@ static o3g_status enqueue_pass(o3g_ctx* c, int blocks, bool write_corr, int32_t*
     CK(cudaStreamIsCapturing(c->exec, &capst));
     const unsigned evflags = capst == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : cudaEventRecordDefault;
     if (ev0) CK(cudaEventRecordWithFlags(ev0, c->exec, evflags));
-    const bool fused = c->world == 1 && k3_variant(c) == 1 && c->n_local > 0;
+    // variant 1 ends its pass in its last block: the A8 epilogue on one GPU,
+    // the rank's slot for the exchange when distributed
+    const bool fused = k3_variant(c) == 1 && c->n_local > 0;
     if (c->estimation) tail_mode |= TAIL_P2P;
     if (phase == 2) {
         launch_tail(nullptr, 0, c->gathered.as<double>(), c->world, c->rank, c->state.as<IcpState>(), hist,
@@ -897,7 +917,9 @@ static o3g_status enqueue_pass(o3g_ctx* c, int blocks, bool write_corr, int32_t*
             ka.part_total = sblocks + blocks;
         }
         if (fused) {
-            ka.fuse_mode = tail_mode;
+            ka.fuse_mode = c->world > 1 ? TAIL_WRITE_RANK : tail_mode;
+            ka.gathered = c->gathered.as<double>();
+            ka.rank = c->rank;
             ka.counter = c->misc.as<unsigned int>() + 12;   // see set_target's misc layout
             ka.st_rw = c->state.as<IcpState>();
             ka.hist_fit = hist.fit;
@@ -912,25 +934,25 @@ static o3g_status enqueue_pass(o3g_ctx* c, int blocks, bool write_corr, int32_t*
     const int nb = c->n_local > 0 ? blocks + (cert && c->cert_sweep ? sblocks : 0) : 0;
     double* gat = c->gathered.as<double>();
     IcpState* st = c->state.as<IcpState>();
-    if (fused) {
+    if (fused && c->world == 1) {
         // A6/A8 ran in the last K3 block
     } else if (c->world == 1) {
         launch_tail(c->partials.as<double>(), nb, gat, 1, 0, st, hist, TAIL_REDUCE_BLOCKS | tail_mode, c->exec);
         ++*nlaunch;
     } else {
-        launch_tail(c->partials.as<double>(), nb, gat, c->world, c->rank, st, TailHist{},
-                    TAIL_REDUCE_BLOCKS | TAIL_WRITE_RANK | (tail_mode & TAIL_STEP), c->exec);
-        if (phase == 1) {
+        if (!fused) {   // (an empty shard still contributes its zero slot)
+            launch_tail(c->partials.as<double>(), nb, gat, c->world, c->rank, st, TailHist{},
+                        TAIL_REDUCE_BLOCKS | TAIL_WRITE_RANK | (tail_mode & TAIL_STEP), c->exec);
             ++*nlaunch;
-            return O3G_OK;
         }
+        if (phase == 1) return O3G_OK;
         if (!c->comm) return fail(O3G_ERR_COMM, "no communicator (a loopback context runs through o3g_loopback_run)");
         nccl_result_t r = nccl().all_gather(gat + (size_t)c->rank * kTermStride, gat, kTermStride,
                                             kNcclFloat64, c->comm, c->exec);
         if (r != 0) return fail(O3G_ERR_COMM, std::string("ncclAllGather: ") +
                                                   (nccl().error_string ? nccl().error_string(r) : "?"));
         launch_tail(nullptr, 0, gat, c->world, c->rank, st, hist, TAIL_SUM_RANKS | tail_mode, c->exec);
-        *nlaunch += 2;
+        *nlaunch += 1;
     }
     return O3G_OK;
 }

@@ -120,7 +120,8 @@ void launch_gather_target(const float* xyz, const float* nrm, const int32_t* val
                           const uint32_t* keys_sorted, int64_t n, float4* tpos, float4* tnrm,
                           unsigned long long* occupied, cudaStream_t s);
 constexpr int kShardBuckets = 4096;   // (grid_build.cu) source-shard histogram buckets
-void launch_key_hist(const uint32_t* keys, int64_t n, int shift, uint32_t* hist, int sms, cudaStream_t s);
+void launch_key_hist(const uint32_t* keys, int64_t n, int shift, const uint32_t* live, uint32_t* hist, int sms,
+                     cudaStream_t s);
 void launch_key_flags(const uint32_t* keys, int64_t n, int shift, uint32_t blo, uint32_t bhi, uint8_t* flags,
                       cudaStream_t s);
 void launch_gather_source(const float* xyz, const int32_t* vals_sorted, int64_t lo, int64_t hi,
@@ -202,8 +203,9 @@ struct K3Args {
     int xsorted;               // target x-sorted inside cells: x-windows in the cooperative path
     int prune;                 // variant 1: row-pruning instantiation (dense grid)
     int prune_min;             //   ... for light queries with >= prune_min candidates
-    // fused tail (single GPU, variant 1): the last block to finish reduces the
-    // block partials in fixed order and runs the A8 epilogue (mode = TAIL_*)
+    // fused tail (variant 1): the last block to finish reduces the block
+    // partials in fixed order and runs the A8 epilogue (mode = TAIL_*), or,
+    // distributed, writes the rank's slot for the exchange
     int fuse_mode;             // 0 = separate k_tail launch
     unsigned int* counter;     // zero between launches (the last block resets it)
     IcpState* st_rw;
@@ -211,6 +213,10 @@ struct K3Args {
     double* hist_rmse;
     double* hist_T;            // per pass: T used and the 29 terms (nullable)
     double* hist_terms;
+    // (world > 1, fuse_mode & TAIL_WRITE_RANK) the last block stores the
+    // rank's 32-slot partial at gathered[rank] instead of finishing the pass
+    double* gathered;
+    int rank;
 };
 constexpr int kCertAges = 32;     // certificates older than this many passes expire
 // variant: 0 = exact fp64 scan (k3_corr_reduce), 1 = two-pass warp kernel

@@ -63,10 +63,12 @@ for P in [int(x) for x in a.worlds.split(",")]:
             k3_ms, k3_n, _ = c.last_run_kernel_ms()
             k3.append(k3_ms)
         if rep:
-            rows.append((max(st), max(ss), max(k3), res.passes, res.fitness))
+            rows.append((max(st), max(ss), max(k3), res.passes, res.fitness, k3))
     for c in ctxs:
         c.close()
     med = lambda i: statistics.median(r[i] for r in rows)
     print(json.dumps({"config": a.config, "world": P, "set_target_ms": med(0), "set_source_ms_max_rank": med(1),
                       "k3_total_ms_max_rank": med(2), "passes": rows[0][3],
-                      "k3_per_pass_ms_max_rank": med(2) / rows[0][3], "fitness": rows[0][4]}), flush=True)
+                      "k3_per_pass_ms_max_rank": med(2) / rows[0][3], "fitness": rows[0][4],
+                      "k3_per_pass_ms_by_rank": [round(x / rows[0][3], 4) for x in rows[-1][5]],
+                      "shard_live_weight": os.environ.get("O3G_SHARD_LIVE_WEIGHT", "8")}), flush=True)

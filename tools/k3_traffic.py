@@ -26,6 +26,11 @@ for row in rows:
     launches.setdefault(int(d["ID"]), {"name": d["Kernel Name"]})[d["Metric Name"]] = (
         float(d["Metric Value"].replace(",", "")), d["Metric Unit"])
 passes, cur = [], None
+# with certificates every pass launches both k3_balanced instantiations (the
+# plain one, then the certificate one; the one not matching the pass's mode
+# exits at once), after k3_sweep in sweep mode: a pass ends at the certificate
+# instantiation; without certificates at each k3_balanced
+certs = any(L["name"].replace(" ", "").rstrip().split("(")[0].endswith(",1>") for L in launches.values())
 for i in sorted(launches):
     L = launches[i]
     t, tu = L["gpu__time_duration.sum"]
@@ -34,10 +39,10 @@ for i in sorted(launches):
         v, u = L[k]
         return v * {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3}.get(u, 1e-6)
     rec = (t, mb("dram__bytes_read.sum") + mb("dram__bytes_write.sum"))
-    if "k3_sweep" in L["name"]:
-        cur = rec
-    elif "k3_balanced" in L["name"]:
-        passes.append((rec[0] + (cur[0] if cur else 0.0), rec[1] + (cur[1] if cur else 0.0)))
+    cur = (rec[0] + (cur[0] if cur else 0.0), rec[1] + (cur[1] if cur else 0.0))
+    ends = "k3_balanced" in L["name"] and (not certs or L["name"].replace(" ", "").rstrip().split("(")[0].endswith(",1>"))
+    if ends:
+        passes.append(cur)
         cur = None
 passes = passes[a.skip:]
 tm = sum(p[0] for p in passes) / len(passes)
@@ -47,7 +52,7 @@ if a.key:
     path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", "k3_traffic.json")
     tab = json.load(open(path)) if os.path.exists(path) else {}
     tab[a.key] = by * 1e6
-    tab["_note"] = ("dram__bytes_read.sum + dram__bytes_write.sum per correspondence pass (k3_balanced, "
-                    "+ k3_sweep with certificates), mean over one registration's passes, ncu --clock-control "
+    tab["_note"] = ("dram__bytes_read.sum + dram__bytes_write.sum per correspondence pass (every k3_ launch "
+                    "of the pass), mean over one registration's passes, ncu --clock-control "
                     "none (tools/k3_traffic.py); keys config@world@regime")
     json.dump(tab, open(path, "w"), indent=1, sort_keys=True)

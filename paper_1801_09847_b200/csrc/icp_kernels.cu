@@ -720,10 +720,12 @@ __global__ void __launch_bounds__(kK3Threads, 4) k3_balanced(const K3Args a) {
         // (certificates) lower bound on d^2 over the stencil rows / cells that were
         // not staged (each was dropped by a bound L > ub on its squared distance)
         float Lskip = CUDART_INF_F;
+        int jkept = -1;   // prev_j[i] as this pass found it (-1 after the run's reset)
         if (i < a.n) {
             p = __ldg(&a.src[i]);
             // previous winner (warm start): the prior pass's, or the certificate's
             const int jprev = warm ? __ldg(&a.prev_j[i]) : -1;   // previous winner (warm start)
+            jkept = jprev;
             xform_rn(sT, p.x, p.y, p.z, sx, sy, sz);
             const int cx = cell_coord(sx, g.ox, g.inv_h, g.nx);
             const int cy = cell_coord(sy, g.oy, g.inv_h, g.ny);
@@ -1150,8 +1152,11 @@ __global__ void __launch_bounds__(kK3Threads, 4) k3_balanced(const K3Args a) {
 #endif
         // decision (exact fp64 rule, R1-R3)
         bool uniq = CERT && !heavy;   // (certificates: the decision had a unique nearest candidate)
+        float4 nspec = make_float4(0.f, 0.f, 0.f, 0.f);   // j1's normal, loaded with its position
+        int jspec = -1;
         if (!heavy && c > 0 && m1 <= thr0) {
             const float4 t = __ldg(&a.tpos[j1]);
+            if (!a.p2p) nspec = __ldg(&a.tnrm[j1]), jspec = j1;
             const double dx = __dsub_rn(sx, (double)t.x), dy = __dsub_rn(sy, (double)t.y),
                          dz = __dsub_rn(sz, (double)t.z);
             const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
@@ -1186,7 +1191,7 @@ __global__ void __launch_bounds__(kK3Threads, 4) k3_balanced(const K3Args a) {
         }
         if (WRITE_CORR && i < a.n) a.corr_out[__float_as_int(p.w)] = widx;
         float4 wn = make_float4(0.f, 0.f, 0.f, 0.f);   // the winner's normal (plane records)
-        if (win >= 0 && !a.p2p) wn = __ldg(&a.tnrm[win]);
+        if (win >= 0 && !a.p2p) wn = win == jspec ? nspec : __ldg(&a.tnrm[win]);
         if (CERT && i < a.n) {
             // certificate of this search: every target other than the winner is at
             // >= L2 (scanned candidates by their prefilter values, unstaged rows /
@@ -1214,9 +1219,10 @@ __global__ void __launch_bounds__(kK3Threads, 4) k3_balanced(const K3Args a) {
             a.cert[2 * (size_t)i] = make_float4(__int_as_float(win), __uint_as_float(cert_pack(gpass, rho, a.inv_h_rd)), wq.x, wq.y);
             if (win >= 0) a.cert[2 * (size_t)i + 1] = make_float4(wq.z, wn.x, wn.y, wn.z);
         }
-        if (a.prev_j && i < a.n) {
-            a.prev_j[i] = win;   // the next pass's warm start
-        }
+        // the next pass's warm start (stored only when it changed: ~98% of the
+        // winners of a pass are the previous pass's, large16m T_init)
+        // (pass 0 of a run finds the buffer reset to -1)
+        if (a.prev_j && i < a.n && (win != jkept || !(warm || (!a.eval_T && a.st->passes == 0)))) a.prev_j[i] = win;
 
         accumulate_records(a, vw, lane, win, sx, sy, sz, wq, wn, wd2, acc0, acc1);
     }

@@ -573,7 +573,7 @@ __global__ void __launch_bounds__(kK3Threads, 4) k3_balanced(const K3Args a) {
     // pass per batch of 32 (s' = T s, cell, one bitmap bit) drops queries
     // whose 27-cell stencil is empty; the rest are queued per warp and the
     // full search runs on full warps of live queries only.
-    __shared__ int qbuf[kK3Threads / 32][64];
+    __shared__ int qbuf[kK3Threads / 32][96];   // (< 32 queued + up to two batches)
     // the live-query pre-pass pays while many queries have nothing in reach;
     // once the previous pass matched at least half of the source it is
     // skipped (measured: large16m queue 0.650 vs 0.733 ms at T_init (fitness
@@ -637,6 +637,50 @@ __global__ void __launch_bounds__(kK3Threads, 4) k3_balanced(const K3Args a) {
                 qn += __popc(lb);
                 __syncwarp();
             }
+          } else if (!CERT && !need && !a.ilv && !g.hashed && a.nbr_bits) {
+        // plain pass, dense grid: two batches per step, so both source loads,
+        // both transforms and both bitmap loads are in flight before either
+        // ballot (the pre-pass is a chain of two dependent loads per batch)
+        while (qn < 32 && base < a.n) {
+            const int ia = base + lane, ib = base + nw * 32 + lane;
+            base += 2 * nw * 32;
+            if (base + lane < a.n) asm volatile("prefetch.global.L1 [%0];" ::"l"(a.src + base + lane));
+            if (base + nw * 32 + lane < a.n) asm volatile("prefetch.global.L1 [%0];" ::"l"(a.src + base + nw * 32 + lane));
+            const float4 pa = ia < a.n ? __ldg(&a.src[ia]) : make_float4(0.f, 0.f, 0.f, 0.f);
+            const float4 pb = ib < a.n ? __ldg(&a.src[ib]) : make_float4(0.f, 0.f, 0.f, 0.f);
+            int ka = -1, kb = -1;
+            {
+                double tx, ty, tz;
+                xform_rn(sT, pa.x, pa.y, pa.z, tx, ty, tz);
+                const int cx = cell_coord(tx, g.ox, g.inv_h, g.nx), cy = cell_coord(ty, g.oy, g.inv_h, g.ny),
+                          cz = cell_coord(tz, g.oz, g.inv_h, g.nz);
+                if (ia < a.n && cx >= -1 && cx <= g.nx && cy >= -1 && cy <= g.ny && cz >= -1 && cz <= g.nz)
+                    ka = (min(max(cz, 0), g.nz - 1) * g.ny + min(max(cy, 0), g.ny - 1)) * g.nx + min(max(cx, 0), g.nx - 1);
+                xform_rn(sT, pb.x, pb.y, pb.z, tx, ty, tz);
+                const int dx = cell_coord(tx, g.ox, g.inv_h, g.nx), dy = cell_coord(ty, g.oy, g.inv_h, g.ny),
+                          dz = cell_coord(tz, g.oz, g.inv_h, g.nz);
+                if (ib < a.n && dx >= -1 && dx <= g.nx && dy >= -1 && dy <= g.ny && dz >= -1 && dz <= g.nz)
+                    kb = (min(max(dz, 0), g.nz - 1) * g.ny + min(max(dy, 0), g.ny - 1)) * g.nx + min(max(dx, 0), g.nx - 1);
+            }
+            const uint32_t wa = ka >= 0 ? __ldg(&a.nbr_bits[ka >> 5]) : 0u;
+            const uint32_t wb = kb >= 0 ? __ldg(&a.nbr_bits[kb >> 5]) : 0u;
+            const bool la = ka >= 0 && ((wa >> (ka & 31)) & 1u), lb2 = kb >= 0 && ((wb >> (kb & 31)) & 1u);
+            if (ia < a.n && !la) {
+                if (WRITE_CORR) a.corr_out[__float_as_int(pa.w)] = -1;
+                if (a.prev_j) a.prev_j[ia] = -1;   // (no winner: no warm start)
+            }
+            if (ib < a.n && !lb2) {
+                if (WRITE_CORR) a.corr_out[__float_as_int(pb.w)] = -1;
+                if (a.prev_j) a.prev_j[ib] = -1;
+            }
+            const unsigned ma = __ballot_sync(0xffffffffu, la);
+            if (la) qbuf[warp][qn + __popc(ma & ((1u << lane) - 1u))] = ia;
+            qn += __popc(ma);
+            const unsigned mb = __ballot_sync(0xffffffffu, lb2);
+            if (lb2) qbuf[warp][qn + __popc(mb & ((1u << lane) - 1u))] = ib;
+            qn += __popc(mb);
+            __syncwarp();
+        }
           } else {
         while (qn < 32 && base < a.n) {
             // interleaved batches (a.ilv = number of batches): lane l of batch b
@@ -698,6 +742,8 @@ __global__ void __launch_bounds__(kK3Threads, 4) k3_balanced(const K3Args a) {
         i = lane < take ? qbuf[warp][lane] : a.n;
         __syncwarp();
         if (lane + 32 < qn) qbuf[warp][lane] = qbuf[warp][lane + 32];
+        __syncwarp();
+        if (lane + 64 < qn) qbuf[warp][lane + 32] = qbuf[warp][lane + 64];
         __syncwarp();
         qn -= take;
         } else {

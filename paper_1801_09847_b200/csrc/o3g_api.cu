@@ -275,14 +275,14 @@ static int bits_for(uint64_t maxval) {
     return b;
 }
 
-static o3g_status sort_pairs(o3g_ctx* c, int64_t n, int end_bit) {
+static o3g_status sort_pairs(o3g_ctx* c, int64_t n, int end_bit, int begin_bit = 0) {
     size_t tmp = 0;
     CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp, c->keys_a.as<uint32_t>(), c->keys_b.as<uint32_t>(),
-                                       c->vals_a.as<int32_t>(), c->vals_b.as<int32_t>(), (int)n, 0,
+                                       c->vals_a.as<int32_t>(), c->vals_b.as<int32_t>(), (int)n, begin_bit,
                                        end_bit, c->exec));
     TRY(c->cub_tmp.ensure(tmp));
     CK(cub::DeviceRadixSort::SortPairs(c->cub_tmp.p, tmp, c->keys_a.as<uint32_t>(), c->keys_b.as<uint32_t>(),
-                                       c->vals_a.as<int32_t>(), c->vals_b.as<int32_t>(), (int)n, 0,
+                                       c->vals_a.as<int32_t>(), c->vals_b.as<int32_t>(), (int)n, begin_bit,
                                        end_bit, c->exec));
     return O3G_OK;
 }
@@ -668,6 +668,7 @@ o3g_status o3g_set_source(o3g_ctx* c, const float* xyz, int64_t n, const double 
     launch_cell_keys(dx, n, c->g, order_T ? T12 : nullptr, c->keys_a.as<uint32_t>(),
                      c->vals_a.as<int32_t>(), c->exec, brick);
     const int kbits = brick ? 32 : bits_for((uint64_t)(c->g.table_size - 1));
+    const int sbits = 0;   // (a 24-bit order of 8-cell x-runs: one sort pass fewer, K3 0.7 % slower, step no faster)
     int64_t lo = (int64_t)c->rank * n / c->world, hi = (int64_t)(c->rank + 1) * n / c->world;
     int64_t base = 0;   // sorted position of the first sorted (selected) key
     if (c->world > 1 && !brick && c->search != 4) {
@@ -722,11 +723,11 @@ o3g_status o3g_set_source(o3g_ctx* c, const float* xyz, int64_t n, const double 
                                           c->vals_b.as<int32_t>(), d_nsel, (int)n, c->exec));
             CK(cudaMemcpyAsync(c->keys_a.p, c->keys_b.p, (size_t)nsel * 4, cudaMemcpyDeviceToDevice, c->exec));
             CK(cudaMemcpyAsync(c->vals_a.p, c->vals_b.p, (size_t)nsel * 4, cudaMemcpyDeviceToDevice, c->exec));
-            TRY(sort_pairs(c, nsel, kbits));
+            TRY(sort_pairs(c, nsel, kbits, sbits));
             c->launches += 7;
         }
     } else {
-        TRY(sort_pairs(c, n, kbits));
+        TRY(sort_pairs(c, n, kbits, sbits));
     }
     TRY(c->src4.ensure((size_t)(hi - lo > 0 ? hi - lo : 1) * sizeof(float4)));
     if (hi > lo) launch_gather_source(dx, c->vals_b.as<int32_t>(), lo - base, hi - base, c->src4.as<float4>(), c->exec);

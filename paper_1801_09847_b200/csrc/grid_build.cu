@@ -165,8 +165,16 @@ __global__ void k_cs_fill(const uint32_t* __restrict__ keys, int64_t n, int64_t 
 // ordering keys (shared-memory privatised, 2^12 buckets), then the stable
 // selection of the keys in a bucket range; sorting only the selection gives
 // exactly the slice of the full stable sort (ties keep original-index order).
-__global__ void k_key_hist(const uint32_t* __restrict__ keys, int64_t n, int shift, const uint32_t* __restrict__ live,
-                           uint32_t* __restrict__ hist) {
+// shard bucket of an ordering key: the top key bits, or (dense grid, nx > 0)
+// the cell's x index scaled to the bucket range, so a shard is an x-slab
+// (every slab of a building-scale scene then holds floor, ceiling and boxes
+// alike; z-slabs put the floor and the ceiling in two cheap shards)
+__device__ __forceinline__ uint32_t shard_bucket(uint32_t k, int shift, int nx) {
+    if (nx > 0) return (uint32_t)(((uint64_t)(k % (uint32_t)nx) * kShardBuckets) / (uint64_t)nx);
+    return min(k >> shift, (uint32_t)kShardBuckets - 1u);
+}
+__global__ void k_key_hist(const uint32_t* __restrict__ keys, int64_t n, int shift, int nx,
+                           const uint32_t* __restrict__ live, uint32_t* __restrict__ hist) {
     // hist[b] = points of bucket b, hist[kShardBuckets + b] = those whose
     // 27-cell stencil holds a target (dense grid: bit `key` of the dilated
     // occupancy bitmap; the live ones run the full search: the work estimate)
@@ -175,7 +183,7 @@ __global__ void k_key_hist(const uint32_t* __restrict__ keys, int64_t n, int shi
     __syncthreads();
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         const uint32_t k = keys[i];
-        const uint32_t b = min(k >> shift, (uint32_t)kShardBuckets - 1u);
+        const uint32_t b = shard_bucket(k, shift, nx);
         atomicAdd(&h[b], 1u);
         if (live && ((__ldg(&live[k >> 5]) >> (k & 31)) & 1u)) atomicAdd(&h[kShardBuckets + b], 1u);
     }
@@ -183,10 +191,10 @@ __global__ void k_key_hist(const uint32_t* __restrict__ keys, int64_t n, int shi
     for (int t = threadIdx.x; t < 2 * kShardBuckets; t += blockDim.x)
         if (h[t]) atomicAdd(&hist[t], h[t]);
 }
-__global__ void k_key_flags(const uint32_t* __restrict__ keys, int64_t n, int shift, uint32_t blo, uint32_t bhi,
-                            uint8_t* __restrict__ flags) {
+__global__ void k_key_flags(const uint32_t* __restrict__ keys, int64_t n, int shift, int nx, uint32_t blo,
+                            uint32_t bhi, uint8_t* __restrict__ flags) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        const uint32_t b = min(keys[i] >> shift, (uint32_t)kShardBuckets - 1u);
+        const uint32_t b = shard_bucket(keys[i], shift, nx);
         flags[i] = (b >= blo && b <= bhi) ? 1 : 0;
     }
 }
@@ -370,14 +378,14 @@ void launch_cs_fill(const uint32_t* keys, int64_t n, int64_t cells, int32_t* cs,
                     cudaStream_t s) {
     k_cs_fill<<<blocks_for(n / 32 + 1, 8), 256, 0, s>>>(keys, n, cells, cs, occ_bits);
 }
-void launch_key_hist(const uint32_t* keys, int64_t n, int shift, const uint32_t* live, uint32_t* hist, int sms,
-                     cudaStream_t s) {
+void launch_key_hist(const uint32_t* keys, int64_t n, int shift, int nx, const uint32_t* live, uint32_t* hist,
+                     int sms, cudaStream_t s) {
     cudaMemsetAsync(hist, 0, 2 * kShardBuckets * sizeof(uint32_t), s);
-    k_key_hist<<<blocks_for(n, 256, sms * 2), 256, 0, s>>>(keys, n, shift, live, hist);
+    k_key_hist<<<blocks_for(n, 256, sms * 2), 256, 0, s>>>(keys, n, shift, nx, live, hist);
 }
-void launch_key_flags(const uint32_t* keys, int64_t n, int shift, uint32_t blo, uint32_t bhi, uint8_t* flags,
-                      cudaStream_t s) {
-    k_key_flags<<<blocks_for(n, 256), 256, 0, s>>>(keys, n, shift, blo, bhi, flags);
+void launch_key_flags(const uint32_t* keys, int64_t n, int shift, int nx, uint32_t blo, uint32_t bhi,
+                      uint8_t* flags, cudaStream_t s) {
+    k_key_flags<<<blocks_for(n, 256), 256, 0, s>>>(keys, n, shift, nx, blo, bhi, flags);
 }
 void launch_coarse_bits(const float4* tpos, int64_t n, const GridDev& g, int shift, int cnx, int cny,
                         uint32_t* bits, cudaStream_t s) {

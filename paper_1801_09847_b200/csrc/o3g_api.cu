@@ -136,6 +136,7 @@ struct o3g_ctx {
     int interleave = -1;  // variant 1 batch interleave: -1 auto, 0 off, 1 on
     int xsort = -1;       // target x-order inside cells: -1 auto, 0 off, 1 on
     double shard_live_weight = 8.0;   // multi-rank split: work of a live query / a dead one
+    bool shard_zslab = false;         // multi-rank split by z-major key ranges instead of x-slabs
     int cert_sweep = 0;   // certificate passes: 0 fused into the search kernel, 1 separate sweep kernel
     int cert_opt = -1;    // correspondence certificates in the run loop: -1 auto, 0 off, 1 on (§5.5)
     int trace_pass = -1;  // o3g_icp_run: record the correspondences of this pass
@@ -325,6 +326,7 @@ o3g_status o3g_create(o3g_ctx** out, int device, void* cuda_stream) {
     c->device = device;
     c->sms = prop.multiProcessorCount;
     if (const char* sw = getenv("O3G_SHARD_LIVE_WEIGHT")) c->shard_live_weight = atof(sw);
+    if (const char* sz = getenv("O3G_SHARD_SLAB")) c->shard_zslab = sz[0] == 'z';
     if (const char* gs = getenv("O3G_CERT_GOAL")) sscanf(gs, "%lf,%lf", &c->rhog_mul, &c->rhog_cap);
     c->user = (cudaStream_t)cuda_stream;
     cudaError_t e = cudaStreamCreate(&c->exec);
@@ -680,9 +682,11 @@ o3g_status o3g_set_source(o3g_ctx* c, const float* xyz, int64_t n, const double 
         // 1.8x the mean work at 8 ranks), then select (stably) and sort only
         // their own buckets. Every rank derives the same split.
         const int shift = kbits > 12 ? kbits - 12 : 0;
+        // dense grid: x-slabs (O3G_SHARD_SLAB=z: z-major key ranges)
+        const int xdiv = c->g.hashed || c->shard_zslab ? 0 : c->g.nx;
         TRY(c->misc2.ensure(2 * kShardBuckets * sizeof(uint32_t)));
         const uint32_t* live = (!c->g.hashed && c->nbr_ready) ? c->nbr_a.as<uint32_t>() : nullptr;
-        launch_key_hist(c->keys_a.as<uint32_t>(), n, shift, live, c->misc2.as<uint32_t>(), c->sms, c->exec);
+        launch_key_hist(c->keys_a.as<uint32_t>(), n, shift, xdiv, live, c->misc2.as<uint32_t>(), c->sms, c->exec);
         std::vector<uint32_t> hist(2 * kShardBuckets);
         CK(cudaMemcpyAsync(hist.data(), c->misc2.p, hist.size() * sizeof(uint32_t), cudaMemcpyDeviceToHost, c->exec));
         CK(cudaStreamSynchronize(c->exec));
@@ -709,7 +713,7 @@ o3g_status o3g_set_source(o3g_ctx* c, const float* xyz, int64_t n, const double 
         lo = before, hi = before + nsel, base = before;
         if (nsel > 0) {
             TRY(c->tflag.ensure((size_t)n + 64));
-            launch_key_flags(c->keys_a.as<uint32_t>(), n, shift, (uint32_t)blo, (uint32_t)bhi,
+            launch_key_flags(c->keys_a.as<uint32_t>(), n, shift, xdiv, (uint32_t)blo, (uint32_t)bhi,
                              c->tflag.as<uint8_t>(), c->exec);
             TRY(c->misc.ensure(128));
             int32_t* d_nsel = (int32_t*)(c->misc.as<uint32_t>() + 20);

@@ -120,10 +120,10 @@ void launch_gather_target(const float* xyz, const float* nrm, const int32_t* val
                           const uint32_t* keys_sorted, int64_t n, float4* tpos, float4* tnrm,
                           unsigned long long* occupied, cudaStream_t s);
 constexpr int kShardBuckets = 4096;   // (grid_build.cu) source-shard histogram buckets
-void launch_key_hist(const uint32_t* keys, int64_t n, int shift, const uint32_t* live, uint32_t* hist, int sms,
-                     cudaStream_t s);
-void launch_key_flags(const uint32_t* keys, int64_t n, int shift, uint32_t blo, uint32_t bhi, uint8_t* flags,
-                      cudaStream_t s);
+void launch_key_hist(const uint32_t* keys, int64_t n, int shift, int nx, const uint32_t* live, uint32_t* hist,
+                     int sms, cudaStream_t s);
+void launch_key_flags(const uint32_t* keys, int64_t n, int shift, int nx, uint32_t blo, uint32_t bhi,
+                      uint8_t* flags, cudaStream_t s);
 void launch_gather_source(const float* xyz, const int32_t* vals_sorted, int64_t lo, int64_t hi,
                           float4* out, cudaStream_t s);
 void launch_fill_i32(int32_t* p, int64_t n, int32_t v, cudaStream_t s);

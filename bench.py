@@ -277,10 +277,13 @@ def main():
         ctx.set_option(2, a.grid)
     if a.bps is not None:
         ctx.set_option(4, a.bps)
+    exchange = "single"
     if world > 1:
-        uid = [o3g.nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(uid, src=0)
-        ctx.dist_init(rank, world, uid[0])
+        # (NCCL all-gather per pass by default; O3G_EXCHANGE=peer: the peer-memory
+        # one-shot exchange, o3g_dist_peer_connect)
+        from paper_1801_09847_b200.dist import exchange_mode, init_distributed
+        exchange = exchange_mode()
+        init_distributed(ctx)
 
     multiscale = "scales" in w
     if multiscale:
@@ -493,6 +496,7 @@ def main():
                        "scales": ([{"voxel": v, "dmax": d, "iters": k} for v, d, k in zip(vox, dms, its)]
                                   if multiscale else None),
                        "parallelism": f"source-shard x{world}, target grid replicated",
+                       "exchange": exchange,
                        "search": ["exact-fp64", "two-pass fp32-prefilter+exact-fp64", "single-pass fp32-prefilter+exact-fp64", "tile-sorted two-pass fp32-prefilter+exact-fp64", "smem-staged-tile two-pass fp32-prefilter+exact-fp64"][a.search],
                        "l2": (f"inputs {in_bytes / 1e6:.0f} MB < 126 MB L2: 256 MB write flushes L2 before "
                               "each timed step" if flush else

@@ -61,7 +61,9 @@ typedef enum {
     O3G_ERR_NOT_IMPLEMENTED = 6
 } o3g_status;
 
-enum { O3G_FLAG_NO_CORRESPONDENCES = 1, O3G_FLAG_DEGENERATE = 2 };
+enum { O3G_FLAG_NO_CORRESPONDENCES = 1, O3G_FLAG_DEGENERATE = 2,
+       O3G_FLAG_COMM_TIMEOUT = 4 /* peer-memory exchange: a rank's partial never arrived; the loop
+                                    stopped with the last T (o3g_dist_peer_connect) */ };
 
 /* Number of reduction terms of one pass (R4):
  * [0..20] J^T J upper triangle, row-major (i <= j); [21..26] J^T r;
@@ -217,6 +219,26 @@ o3g_status o3g_icp_multiscale(o3g_ctx* ctx, const float* source_xyz, int64_t n_s
 o3g_status o3g_nccl_unique_id(void* id_out_128);
 o3g_status o3g_dist_init(o3g_ctx* ctx, int rank, int world, const void* nccl_unique_id_128);
 
+/* Peer-memory exchange (SURVEY §8(e) "fused one-shot exchange"; replaces the
+ * per-pass NCCL all-gather): each rank owns a small exchange buffer in device
+ * memory; the last block of a rank's correspondence kernel stores its 29-term
+ * partial straight into EVERY rank's buffer (peer stores over NVLink) and
+ * releases a per-pass epoch flag there; the rank's tail kernel acquires the
+ * world flags of its own buffer, sums the slots in rank order and runs the A8
+ * update — two kernels per pass, no collective call, T bit-identical on every
+ * rank as with the all-gather. Setup (after o3g_dist_init with world > 1, all
+ * ranks on one node with peer access): every rank calls o3g_dist_peer_handle
+ * (64 bytes out, host: the CUDA IPC handle of its buffer), the caller
+ * all-gathers the handles (e.g. torch.distributed) and every rank passes the
+ * world x 64 bytes (rank order) to o3g_dist_peer_connect. Every rank must make
+ * the same sequence of step/run calls (the epochs count them). A rank whose
+ * peers never arrive stops after 20 s with O3G_FLAG_COMM_TIMEOUT instead of
+ * hanging. O3G_ERR_COMM if a handle cannot be opened (no peer access);
+ * o3g_dist_init drops the connection.                                     */
+#define O3G_PEER_HANDLE_BYTES 64
+o3g_status o3g_dist_peer_handle(o3g_ctx* ctx, void* handle_out_64);
+o3g_status o3g_dist_peer_connect(o3g_ctx* ctx, const void* handles_world_x_64);
+
 /* In-process loopback of the multi-GPU path (verification of SURVEY §8(e)
  * A7 on one device): o3g_dist_init_loopback makes ctx rank `rank` of `world`
  * WITHOUT a communicator (call it before o3g_set_source, which then keeps the
@@ -231,6 +253,12 @@ o3g_status o3g_dist_init(o3g_ctx* ctx, int rank, int world, const void* nccl_uni
  * transforms ever differ (they must be bit-identical). o3g_last_run_trace
  * works on each context afterwards.                                      */
 o3g_status o3g_dist_init_loopback(o3g_ctx* ctx, int rank, int world);
+/* Loopback with the peer-memory exchange: wires the world loopback contexts'
+ * exchange buffers to one another (plain device pointers instead of IPC
+ * mappings); o3g_loopback_run then runs every rank's publishing kernels
+ * before any rank's waiting tail, so the waits are already satisfied and no
+ * kernel on the device ever waits for a later one.                        */
+o3g_status o3g_loopback_peer_connect(o3g_ctx* const* ctxs, int world);
 o3g_status o3g_loopback_run(o3g_ctx* const* ctxs, int world, const double init_T[16],
                             int32_t max_iterations, double relative_fitness, double relative_rmse,
                             double T_out[16], double* fitness, double* inlier_rmse, o3g_icp_info* info);

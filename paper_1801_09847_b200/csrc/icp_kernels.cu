@@ -227,6 +227,47 @@ __device__ __forceinline__ int warp_bound_x(const float4* __restrict__ tpos, int
     return lo + __popc(__ballot_sync(0xffffffffu, p < hi && (GE ? x < v : x <= v)));
 }
 
+// ---- peer-memory rank exchange (TAIL_PEER; Xchg in o3g_internal.cuh)
+__device__ __forceinline__ void st_release_sys(unsigned int* p, unsigned int v) {
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned int ld_acquire_sys(const unsigned int* p) {
+    unsigned int v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+// The whole block: store this rank's 32-slot partial (terms, shared memory)
+// into every rank's buffer, then release the epoch flag there (stores,
+// system-scope fence, block barrier, release store: a rank that acquires the
+// flag sees the slots).
+__device__ __forceinline__ void xchg_publish(Xchg* const* peers, int world, int rank, const double* terms,
+                                             unsigned int epoch) {
+    const int par = epoch & 1u;
+    for (int idx = threadIdx.x; idx < world * kTermStride; idx += blockDim.x) {
+        const int q = idx / kTermStride, t = idx % kTermStride;
+        peers[q]->slots[par][rank][t] = t < kTermsStats ? terms[t] : 0.0;
+    }
+    __threadfence_system();
+    __syncthreads();
+    for (int q = threadIdx.x; q < world; q += blockDim.x) st_release_sys(&peers[q]->flags[par][rank], epoch);
+}
+// Thread r < world waits for rank r's flag of this epoch in this rank's own
+// buffer; false after kXchgTimeoutNs (a lost peer must not hang the GPU).
+constexpr unsigned long long kXchgTimeoutNs = 20ull * 1000ull * 1000ull * 1000ull;
+__device__ __forceinline__ bool xchg_wait(const Xchg* self, int r, unsigned int epoch) {
+    const unsigned int* f = &self->flags[epoch & 1u][r];
+    if (ld_acquire_sys(f) == epoch) return true;
+    unsigned long long t0, t1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    for (;;) {
+        for (int k = 0; k < 64; ++k)
+            if (ld_acquire_sys(f) == epoch) return true;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+        if (t1 - t0 > kXchgTimeoutNs) return false;
+        __nanosleep(200);
+    }
+}
+
 __device__ __noinline__ void tail_finish(const double* terms, IcpState* st, const TailHist& hist, int mode);
 
 // ------------------------------------------- correspondence certificates
@@ -1333,8 +1374,13 @@ __global__ void __launch_bounds__(kK3Threads, 4) k3_balanced(const K3Args a) {
     }
     __syncthreads();
     if (a.fuse_mode & TAIL_WRITE_RANK) {   // (distributed: this rank's slot; the exchange and the solve follow)
-        if (threadIdx.x < kTermStride) a.gathered[a.rank * kTermStride + threadIdx.x] = terms[threadIdx.x];
         if (threadIdx.x == 0) *a.counter = 0u;
+        if (a.fuse_mode & TAIL_PEER) {
+            // one-shot exchange: the slot goes straight into every rank's buffer
+            xchg_publish(a.xpeers, a.world, a.rank, terms, a.st->xbase + (unsigned int)a.st->passes + 1u);
+            return;
+        }
+        if (threadIdx.x < kTermStride) a.gathered[a.rank * kTermStride + threadIdx.x] = terms[threadIdx.x];
         return;
     }
     if (threadIdx.x == 0) {
@@ -1808,9 +1854,11 @@ __device__ __noinline__ void tail_finish(const double* terms, IcpState* st, cons
 
 __global__ void __launch_bounds__(kTailThreads)
     k_tail(const double* __restrict__ partials, int nblocks, double* gathered, int world, int rank,
-           IcpState* st, TailHist hist, int mode) {
+           IcpState* st, TailHist hist, int mode, Xchg* const* xpeers) {
     __shared__ double terms[kTermStride];
+    __shared__ int s_lost;
     if (!(mode & TAIL_STEP) && st->done) return;
+    const unsigned int epoch = st->xbase + (unsigned int)st->passes + 1u;   // (TAIL_PEER)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (mode & TAIL_REDUCE_BLOCKS) {
         if (warp < kTermsStats) {
@@ -1822,15 +1870,33 @@ __global__ void __launch_bounds__(kTailThreads)
         }
         __syncthreads();
         if (mode & TAIL_WRITE_RANK) {
+            if (mode & TAIL_PEER) {
+                xchg_publish(xpeers, world, rank, terms, epoch);
+                return;
+            }
             if (threadIdx.x < kTermStride)
                 gathered[rank * kTermStride + threadIdx.x] = threadIdx.x < kTermsStats ? terms[threadIdx.x] : 0.0;
             return;
         }
     }
     if (mode & TAIL_SUM_RANKS) {
+        const double* slots = gathered;
+        if (mode & TAIL_PEER) {
+            // wait for every rank's flag of this pass in this rank's buffer
+            const Xchg* self = xpeers[rank];
+            if (threadIdx.x == 0) s_lost = 0;
+            __syncthreads();
+            if (threadIdx.x < world && !xchg_wait(self, threadIdx.x, epoch)) s_lost = 1;
+            __syncthreads();
+            if (s_lost) {   // a peer never arrived: stop the loop on this rank, T unchanged
+                if (threadIdx.x == 0) st->flags |= 4 /* O3G_FLAG_COMM_TIMEOUT */, st->done = 1;
+                return;
+            }
+            slots = &self->slots[epoch & 1u][0][0];
+        }
         if (threadIdx.x < kTermsStats) {
             double s = 0.0;
-            for (int r = 0; r < world; ++r) s += gathered[r * kTermStride + threadIdx.x];
+            for (int r = 0; r < world; ++r) s += __ldcg(&slots[r * kTermStride + threadIdx.x]);
             terms[threadIdx.x] = s;
         }
         __syncthreads();
@@ -1868,8 +1934,8 @@ void launch_eval_reduce(const double* partials, int nblocks, int k, double n_tot
 }
 
 void launch_tail(const double* partials, int nblocks, double* gathered, int world, int rank,
-                 IcpState* st, TailHist hist, int mode, cudaStream_t s) {
-    k_tail<<<1, kTailThreads, 0, s>>>(partials, nblocks, gathered, world, rank, st, hist, mode);
+                 IcpState* st, TailHist hist, int mode, cudaStream_t s, Xchg* const* xpeers) {
+    k_tail<<<1, kTailThreads, 0, s>>>(partials, nblocks, gathered, world, rank, st, hist, mode, xpeers);
 }
 
 }  // namespace o3g

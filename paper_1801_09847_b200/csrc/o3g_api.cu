@@ -189,6 +189,12 @@ struct o3g_ctx {
     int rank = 0, world = 1;
     bool loopback = false;         // o3g_dist_init_loopback: no communicator (o3g_loopback_run)
     nccl_comm_t comm = nullptr;
+    // peer-memory exchange (o3g_dist_peer_*): this rank's Xchg, the device array of
+    // every rank's Xchg pointer, and the peers' buffers opened through CUDA IPC
+    DevBuf xchg, xpeers;
+    std::vector<void*> ipc_opened;
+    bool peer_xchg = false;
+    uint32_t xepoch = 0;           // the next run's IcpState::xbase
     // stats
     int64_t launches = 0;
     double last_k3_ms = 0.0, last_tail_ms = 0.0;
@@ -341,6 +347,15 @@ o3g_status o3g_create(o3g_ctx** out, int device, void* cuda_stream) {
     return O3G_OK;
 }
 
+// drop the peer-memory exchange (IPC mappings and the pointer table; the
+// context's own Xchg buffer stays allocated so an exported handle stays valid)
+static void peer_disconnect(o3g_ctx* c) {
+    for (void* p : c->ipc_opened) cudaIpcCloseMemHandle(p);
+    c->ipc_opened.clear();
+    c->xpeers.release();
+    c->peer_xchg = false;
+}
+
 o3g_status o3g_destroy(o3g_ctx* c) {
     if (!c) return O3G_OK;
     cudaSetDevice(c->device);
@@ -354,6 +369,8 @@ o3g_status o3g_destroy(o3g_ctx* c) {
                       &c->ms_tgt, &c->ms_nrm, &c->ev_T, &c->ev_part, &c->ev_out, &c->tiles, &c->tflag, &c->prevj, &c->ms_in_src, &c->ms_in_tgt, &c->ms_in_nrm, &c->xk_a, &c->xk_b, &c->xpos, &c->xnrm, &c->cert, &c->hist_T, &c->hist_terms, &c->trace_corr, &c->nbr_c, &c->need};
     for (DevBuf* b : bufs) b->release();
     if (c->comm && nccl().comm_destroy) nccl().comm_destroy(c->comm);
+    peer_disconnect(c);
+    c->xchg.release();
     if (c->h_state) cudaFreeHost(c->h_state);
     if (c->fence) cudaEventDestroy(c->fence);
     for (cudaEvent_t e : c->ev_copy)
@@ -902,9 +919,14 @@ static o3g_status enqueue_pass(o3g_ctx* c, int blocks, bool write_corr, int32_t*
     // the rank's slot for the exchange when distributed
     const bool fused = k3_variant(c) == 1 && c->n_local > 0;
     if (c->estimation) tail_mode |= TAIL_P2P;
+    // rank exchange through peer memory (o3g_dist_peer_connect / the loopback's
+    // peer transport): K3's last block publishes to every rank, the tail waits
+    const bool peer = c->world > 1 && c->peer_xchg;
+    Xchg* const* xp = peer ? c->xpeers.as<Xchg*>() : nullptr;
+    const int xmode = peer ? TAIL_PEER : 0;
     if (phase == 2) {
         launch_tail(nullptr, 0, c->gathered.as<double>(), c->world, c->rank, c->state.as<IcpState>(), hist,
-                    TAIL_SUM_RANKS | tail_mode, c->exec);
+                    TAIL_SUM_RANKS | tail_mode | xmode, c->exec, xp);
         ++*nlaunch;
         return O3G_OK;
     }
@@ -922,9 +944,11 @@ static o3g_status enqueue_pass(o3g_ctx* c, int blocks, bool write_corr, int32_t*
             ka.part_total = sblocks + blocks;
         }
         if (fused) {
-            ka.fuse_mode = c->world > 1 ? TAIL_WRITE_RANK : tail_mode;
+            ka.fuse_mode = c->world > 1 ? (TAIL_WRITE_RANK | xmode) : tail_mode;
             ka.gathered = c->gathered.as<double>();
             ka.rank = c->rank;
+            ka.xpeers = xp;
+            ka.world = c->world;
             ka.counter = c->misc.as<unsigned int>() + 12;   // see set_target's misc layout
             ka.st_rw = c->state.as<IcpState>();
             ka.hist_fit = hist.fit;
@@ -947,16 +971,18 @@ static o3g_status enqueue_pass(o3g_ctx* c, int blocks, bool write_corr, int32_t*
     } else {
         if (!fused) {   // (an empty shard still contributes its zero slot)
             launch_tail(c->partials.as<double>(), nb, gat, c->world, c->rank, st, TailHist{},
-                        TAIL_REDUCE_BLOCKS | TAIL_WRITE_RANK | (tail_mode & TAIL_STEP), c->exec);
+                        TAIL_REDUCE_BLOCKS | TAIL_WRITE_RANK | (tail_mode & TAIL_STEP) | xmode, c->exec, xp);
             ++*nlaunch;
         }
         if (phase == 1) return O3G_OK;
-        if (!c->comm) return fail(O3G_ERR_COMM, "no communicator (a loopback context runs through o3g_loopback_run)");
-        nccl_result_t r = nccl().all_gather(gat + (size_t)c->rank * kTermStride, gat, kTermStride,
-                                            kNcclFloat64, c->comm, c->exec);
-        if (r != 0) return fail(O3G_ERR_COMM, std::string("ncclAllGather: ") +
-                                                  (nccl().error_string ? nccl().error_string(r) : "?"));
-        launch_tail(nullptr, 0, gat, c->world, c->rank, st, hist, TAIL_SUM_RANKS | tail_mode, c->exec);
+        if (!peer) {
+            if (!c->comm) return fail(O3G_ERR_COMM, "no communicator (a loopback context runs through o3g_loopback_run)");
+            nccl_result_t r = nccl().all_gather(gat + (size_t)c->rank * kTermStride, gat, kTermStride,
+                                                kNcclFloat64, c->comm, c->exec);
+            if (r != 0) return fail(O3G_ERR_COMM, std::string("ncclAllGather: ") +
+                                                      (nccl().error_string ? nccl().error_string(r) : "?"));
+        }
+        launch_tail(nullptr, 0, gat, c->world, c->rank, st, hist, TAIL_SUM_RANKS | tail_mode | xmode, c->exec, xp);
         *nlaunch += 1;
     }
     return O3G_OK;
@@ -982,6 +1008,10 @@ static void init_state(o3g_ctx* c, const double* T, int max_it, double ef, doubl
     }
     s->gbase = c->cert_epoch;
     c->cert_epoch += max_it + 1;
+    // peer-memory exchange: pass p of this run carries epoch xbase + p + 1 (never 0,
+    // the cleared flag value; every rank makes the same calls, so the same epochs)
+    s->xbase = c->xepoch;
+    c->xepoch += (uint32_t)max_it + 2u;
 }
 
 o3g_status o3g_icp_step(o3g_ctx* c, const double T_in[16], int32_t* corr_out, double JTJ_out[36],
@@ -1255,6 +1285,7 @@ o3g_status o3g_dist_init(o3g_ctx* c, int rank, int world, const void* id) {
     invalidate_graph(c);
     c->src_ready = false;
     c->loopback = false;
+    peer_disconnect(c);
     if (c->comm && nccl().comm_destroy) nccl().comm_destroy(c->comm);
     c->comm = nullptr;
     c->rank = rank;
@@ -1281,6 +1312,87 @@ o3g_status o3g_dist_init_loopback(o3g_ctx* c, int rank, int world) {
     c->rank = rank;
     c->world = world;
     c->loopback = world > 1;
+    return O3G_OK;
+}
+
+// this rank's exchange buffer: allocated once, zeroed (flag 0 = no epoch)
+static o3g_status xchg_ensure(o3g_ctx* c) {
+    if (c->xchg.p) return O3G_OK;
+    TRY(c->xchg.ensure(sizeof(Xchg)));
+    CK(cudaMemset(c->xchg.p, 0, sizeof(Xchg)));
+    CK(cudaDeviceSynchronize());   // (cleared before any peer can learn the handle)
+    return O3G_OK;
+}
+
+// install the table of every rank's Xchg pointer and switch the exchange over
+static o3g_status peer_install(o3g_ctx* c, const std::vector<Xchg*>& table) {
+    TRY(c->xpeers.ensure(table.size() * sizeof(Xchg*)));
+    CK(cudaMemcpy(c->xpeers.p, table.data(), table.size() * sizeof(Xchg*), cudaMemcpyHostToDevice));
+    invalidate_graph(c);
+    // (epochs keep growing over the context's life, so flags left by earlier
+    // runs are always below the next run's: no reset, hence no race with a
+    // peer that already publishes into this rank's buffer)
+    c->peer_xchg = true;
+    return O3G_OK;
+}
+
+o3g_status o3g_dist_peer_handle(o3g_ctx* c, void* handle_out_64) {
+    if (!c || !handle_out_64) return fail(O3G_ERR_INVALID_ARGUMENT, "ctx or handle_out is NULL");
+    static_assert(sizeof(cudaIpcMemHandle_t) == O3G_PEER_HANDLE_BYTES, "IPC handle size");
+    CK(cudaSetDevice(c->device));
+    TRY(xchg_ensure(c));
+    cudaIpcMemHandle_t h;
+    CK(cudaIpcGetMemHandle(&h, c->xchg.p));
+    memcpy(handle_out_64, &h, sizeof(h));
+    return O3G_OK;
+}
+
+o3g_status o3g_dist_peer_connect(o3g_ctx* c, const void* handles) {
+    if (!c) return fail(O3G_ERR_INVALID_ARGUMENT, "ctx is NULL");
+    if (c->world < 2 || c->loopback) return fail(O3G_ERR_INVALID_ARGUMENT, "o3g_dist_init with world > 1 first");
+    if (c->world > kMaxWorld) return fail(O3G_ERR_INVALID_ARGUMENT, "peer exchange supports up to 64 ranks");
+    if (!handles) return fail(O3G_ERR_INVALID_ARGUMENT, "handles is NULL");
+    CK(cudaSetDevice(c->device));
+    TRY(xchg_ensure(c));
+    peer_disconnect(c);
+    std::vector<Xchg*> table(c->world);
+    for (int r = 0; r < c->world; ++r) {
+        if (r == c->rank) {
+            table[r] = c->xchg.as<Xchg>();
+            continue;
+        }
+        cudaIpcMemHandle_t h;
+        memcpy(&h, (const char*)handles + (size_t)r * sizeof(h), sizeof(h));
+        void* p = nullptr;
+        cudaError_t e = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            peer_disconnect(c);
+            return fail(O3G_ERR_COMM, std::string("cudaIpcOpenMemHandle (rank ") + std::to_string(r) + "): " +
+                                          cudaGetErrorString(e));
+        }
+        c->ipc_opened.push_back(p);
+        table[r] = (Xchg*)p;
+    }
+    return peer_install(c, table);
+}
+
+o3g_status o3g_loopback_peer_connect(o3g_ctx* const* ctxs, int world) {
+    if (!ctxs || world < 2 || world > kMaxWorld) return fail(O3G_ERR_INVALID_ARGUMENT, "need 2 <= world <= 64 contexts");
+    std::vector<Xchg*> table(world);
+    for (int r = 0; r < world; ++r) {
+        o3g_ctx* c = ctxs[r];
+        if (!c || c->rank != r || c->world != world || !c->loopback)
+            return fail(O3G_ERR_INVALID_ARGUMENT, "ctxs[r] must be loopback rank r of world");
+        if (c->device != ctxs[0]->device) return fail(O3G_ERR_INVALID_ARGUMENT, "loopback contexts share one device");
+        CK(cudaSetDevice(c->device));
+        TRY(xchg_ensure(c));
+        table[r] = c->xchg.as<Xchg>();
+    }
+    for (int r = 0; r < world; ++r) {
+        peer_disconnect(ctxs[r]);
+        TRY(peer_install(ctxs[r], table));
+    }
     return O3G_OK;
 }
 
@@ -1346,7 +1458,9 @@ o3g_status o3g_loopback_run(o3g_ctx* const* ctxs, int world, const double init_T
             }
             if (world == 1) continue;
             // the transport: rank r's slot of its gathered buffer -> every other rank's
-            for (int r = 0; r < world; ++r)
+            // (peer transport: every rank's K3 already stored its slot into every
+            // rank's Xchg and released its flag, so the tails below never spin)
+            for (int r = 0; r < world && !ctxs[0]->peer_xchg; ++r)
                 for (int q = 0; q < world; ++q)
                     if (q != r)
                         CK(cudaMemcpyAsync(ctxs[q]->gathered.as<double>() + (size_t)r * kTermStride,

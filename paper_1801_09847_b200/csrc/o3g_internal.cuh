@@ -50,6 +50,21 @@ struct IcpState {
                      // run is older than the current pass index, hence invalid; the host
                      // advances gbase per run and requests a reset (creset) on wrap-around
     int32_t creset;  // 1: k_cert_reset clears the records at the head of this run
+    uint32_t xbase;  // peer-memory exchange: pass p of this run carries epoch xbase + p + 1
+                     // (the host advances it per run, identically on every rank)
+};
+
+// Peer-memory exchange buffer of one rank (TAIL_PEER; SURVEY §8(e) "fused
+// one-shot exchange"): rank r's last K3 block stores its 32-slot partial into
+// slots[epoch & 1][r] of EVERY rank's buffer (peer stores over NVLink), then
+// releases flags[epoch & 1][r] = epoch there; the rank's tail kernel acquires
+// its own world flags and sums the slots in rank order. Two parities: a rank
+// can run at most one pass ahead of the slowest reader (its pass p + 2 needs
+// every rank's flag of pass p + 1, set after that rank's tail of pass p).
+constexpr int kMaxWorld = 64;
+struct Xchg {
+    double slots[2][kMaxWorld][kTermStride];
+    unsigned int flags[2][kMaxWorld];
 };
 
 enum TailMode : int {
@@ -59,6 +74,8 @@ enum TailMode : int {
     TAIL_SOLVE = 8,          // criteria + LDLT + exp + T update (A8)
     TAIL_STEP = 16,          // store terms only (o3g_icp_step)
     TAIL_P2P = 32,           // point-to-point estimation (Horn's quaternion fit)
+    TAIL_PEER = 64,          // rank exchange through peer memory (Xchg) instead of gathered[]:
+                             // WRITE_RANK publishes to every rank, SUM_RANKS waits for all flags
 };
 
 __host__ __device__ inline int64_t grid_index_dense(const GridDev& g, int cx, int cy, int cz) {
@@ -217,6 +234,10 @@ struct K3Args {
     // rank's 32-slot partial at gathered[rank] instead of finishing the pass
     double* gathered;
     int rank;
+    // (fuse_mode & TAIL_PEER) peer-memory exchange: xpeers[q] = rank q's Xchg
+    // (this rank's own buffer at [rank]; a device array of world pointers)
+    Xchg* const* xpeers;
+    int world;
 };
 constexpr int kCertAges = 32;     // certificates older than this many passes expire
 // variant: 0 = exact fp64 scan (k3_corr_reduce), 1 = two-pass warp kernel
@@ -242,6 +263,6 @@ struct TailHist {
     double* terms;   // [pass][kTermStride]
 };
 void launch_tail(const double* block_partials, int nblocks, double* gathered, int world, int rank,
-                 IcpState* st, TailHist hist, int mode, cudaStream_t s);
+                 IcpState* st, TailHist hist, int mode, cudaStream_t s, Xchg* const* xpeers = nullptr);
 
 }  // namespace o3g

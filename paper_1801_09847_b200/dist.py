@@ -32,8 +32,34 @@ def broadcast_unique_id(make_id, group=None) -> bytes:
     return bytes(uid)
 
 
-def init_distributed(ctx, group=None, make_id=None):
-    """o3g_dist_init on `ctx` with this process's rank/world."""
+def gather_peer_handles(handle: bytes, group=None) -> bytes:
+    """All ranks' 64-byte exchange-buffer handles in rank order (the
+    bootstrap of o3g_dist_peer_connect)."""
+    import torch.distributed as dist
+    if not isinstance(handle, (bytes, bytearray)) or len(handle) != 64:
+        raise RuntimeError("bad peer handle")
+    out = [None] * dist.get_world_size(group)
+    dist.all_gather_object(out, bytes(handle), group=group)
+    if any(not isinstance(h, (bytes, bytearray)) or len(h) != 64 for h in out):
+        raise RuntimeError("bad peer handle from a rank")
+    return b"".join(out)
+
+
+def exchange_mode(exchange=None) -> str:
+    """'nccl' (default: the graph-captured all-gather) or 'peer' (the
+    peer-memory one-shot exchange); O3G_EXCHANGE overrides the default."""
+    import os
+    mode = exchange or os.environ.get("O3G_EXCHANGE", "nccl")
+    if mode not in ("nccl", "peer"):
+        raise ValueError("exchange must be 'nccl' or 'peer'")
+    return mode
+
+
+def init_distributed(ctx, group=None, make_id=None, exchange=None):
+    """o3g_dist_init on `ctx` with this process's rank/world; with
+    exchange='peer' (or O3G_EXCHANGE=peer) also o3g_dist_peer_connect: the
+    ranks swap the IPC handles of their exchange buffers and a barrier makes
+    sure every rank is connected before any pass publishes."""
     import torch.distributed as dist
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
@@ -43,3 +69,6 @@ def init_distributed(ctx, group=None, make_id=None):
     if make_id is None:
         from .o3g import nccl_unique_id as make_id
     ctx.dist_init(rank, world, broadcast_unique_id(make_id, group))
+    if exchange_mode(exchange) == "peer":
+        ctx.dist_peer_connect(gather_peer_handles(ctx.dist_peer_handle(), group))
+        dist.barrier(group)

@@ -72,6 +72,9 @@ def lib() -> C.CDLL:
             "o3g_dist_init": [P, C.c_int, C.c_int, P],
             "o3g_dist_init_loopback": [P, C.c_int, C.c_int],
             "o3g_loopback_run": [P, C.c_int, P, I32, D, D, P, P, P, P],
+            "o3g_loopback_peer_connect": [P, C.c_int],
+            "o3g_dist_peer_handle": [P, P],
+            "o3g_dist_peer_connect": [P, P],
             "o3g_set_option": [P, C.c_int, I64],
             "o3g_last_run_kernel_ms": [P, P, P, P],
             "o3g_last_run_trace": [P, P, P, P, P],
@@ -213,6 +216,14 @@ def loopback_run(ctxs, init=None, max_iterations=30, relative_fitness=1e-6,
     return _result(T, fit, rmse, info)
 
 
+def loopback_peer_connect(ctxs) -> None:
+    """o3g_loopback_peer_connect: the loopback world exchanges through the
+    peer-memory transport (each rank's kernel stores into every rank's
+    exchange buffer) instead of device copies of the gathered slots."""
+    arr = (C.c_void_p * len(ctxs))(*[c._h.value for c in ctxs])
+    _check(lib().o3g_loopback_peer_connect(arr, len(ctxs)))
+
+
 def nccl_unique_id() -> bytes:
     buf = C.create_string_buffer(128)
     _check(lib().o3g_nccl_unique_id(buf))
@@ -267,6 +278,20 @@ class Context:
         buf = C.create_string_buffer(unique_id, 128) if unique_id is not None else None
         _check(lib().o3g_dist_init(self._h, int(rank), int(world), buf))
         self.rank, self.world = rank, world
+
+    def dist_peer_handle(self) -> bytes:
+        """o3g_dist_peer_handle: the 64-byte CUDA IPC handle of this rank's
+        exchange buffer."""
+        buf = C.create_string_buffer(64)
+        _check(lib().o3g_dist_peer_handle(self._h, buf))
+        return buf.raw
+
+    def dist_peer_connect(self, handles: bytes):
+        """o3g_dist_peer_connect: world x 64 bytes, the ranks' handles in rank
+        order; the per-pass exchange then runs through peer memory."""
+        if len(handles) != 64 * self.world:
+            raise ValueError("handles must hold 64 bytes per rank")
+        _check(lib().o3g_dist_peer_connect(self._h, C.create_string_buffer(handles, len(handles))))
 
     def dist_init_loopback(self, rank: int, world: int):
         """o3g_dist_init_loopback: rank `rank` of an in-process world (no

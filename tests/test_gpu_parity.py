@@ -644,8 +644,8 @@ def test_run_loop_state_reset_between_runs(o3g, workloads):
 
 
 # ------------------------------------------------ A7: the multi-rank path (loopback)
-@pytest.mark.parametrize("world", [2, 4, 8])
-def test_loopback_multi_rank(o3g, workloads, world):
+@pytest.mark.parametrize("world,transport", [(2, "copy"), (4, "copy"), (8, "copy"), (2, "peer"), (8, "peer")])
+def test_loopback_multi_rank(o3g, workloads, world, transport):
     """SURVEY §8(e) / A7 on one device: P contexts, each keeping its contiguous
     shard of the spatially ordered source, run the distributed loop in
     lockstep — per-shard correspondence kernels, TAIL_WRITE_RANK, the slot
@@ -654,7 +654,11 @@ def test_loopback_multi_rank(o3g, workloads, world):
     equals the 1-GPU pass bit for bit at every traced pass; every pass's
     rank-summed terms agree with the 1-GPU pass (R14) and with the oracle at
     that T; T is bit-identical on every rank (checked inside the call) and
-    the loop matches the oracle's (1e-6)."""
+    the loop matches the oracle's (1e-6). transport "peer": the one-shot
+    peer-memory exchange (each rank's last K3 block stores its slot into every
+    rank's exchange buffer and releases the pass's epoch flag; the tails
+    acquire the flags) instead of copies of the gathered slots; several runs
+    on the same contexts exercise both parities and growing epochs."""
     w = workloads("large16m", n=400_000)
     T0 = w["T_true"] @ _perturb(61, 0.004, 0.01)
     iters = 6
@@ -677,6 +681,8 @@ def test_loopback_multi_rank(o3g, workloads, world):
                 c.dist_init_loopback(rk, world)
                 c.set_source(_dev(w["source"]), T0)
                 ctxs.append(c)
+            if transport == "peer":
+                o3g.loopback_peer_connect(ctxs)
             rp = o3g.loopback_run(ctxs, T0, iters, 0.0, 0.0)
             assert rp.passes == r1.passes and rp.iterations == r1.iterations
             assert np.abs(rp.transformation - ref["T"]).max() <= 1e-6, cert

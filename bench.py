@@ -56,6 +56,7 @@ def parse():
                     help="start from the config's init T (default) or from T* perturbed by 0.1 deg / 1 cm "
                          "(SURVEY 8(d) 'converged-regime' run)")
     ap.add_argument("--bps", type=int, default=None, help="override O3G_OPT_BLOCKS_PER_SM")
+    ap.add_argument("--cert", type=int, default=None, help="override O3G_OPT_CERT (-1 auto, 0 off, 1 on, 2 forced)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--n", type=int, default=None, help="override point count (testing only)")
@@ -277,6 +278,8 @@ def main():
         ctx.set_option(2, a.grid)
     if a.bps is not None:
         ctx.set_option(4, a.bps)
+    if a.cert is not None:
+        ctx.set_option(13, a.cert)
     exchange = "single"
     if world > 1:
         # (NCCL all-gather per pass by default; O3G_EXCHANGE=peer: the peer-memory

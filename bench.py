@@ -57,6 +57,8 @@ def parse():
                          "(SURVEY 8(d) 'converged-regime' run)")
     ap.add_argument("--bps", type=int, default=None, help="override O3G_OPT_BLOCKS_PER_SM")
     ap.add_argument("--cert", type=int, default=None, help="override O3G_OPT_CERT (-1 auto, 0 off, 1 on, 2 forced)")
+    ap.add_argument("--nccl-one-rank", action="store_true",
+                    help="N=1 only: run the distributed pass (rank slot, ncclAllGather, rank-order tail) on a one-rank communicator")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--n", type=int, default=None, help="override point count (testing only)")
@@ -281,6 +283,9 @@ def main():
     if a.cert is not None:
         ctx.set_option(13, a.cert)
     exchange = "single"
+    if world == 1 and a.nccl_one_rank:
+        exchange = "nccl (one-rank communicator)"
+        ctx.dist_init(0, 1, o3g.nccl_unique_id())
     if world > 1:
         # (NCCL all-gather per pass by default; O3G_EXCHANGE=peer: the peer-memory
         # one-shot exchange, o3g_dist_peer_connect)

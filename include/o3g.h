@@ -215,7 +215,11 @@ o3g_status o3g_icp_multiscale(o3g_ctx* ctx, const float* source_xyz, int64_t n_s
  * o3g_dist_init before o3g_set_source. Each pass then all-gathers the 29
  * partial terms of every rank (232 B + padding per rank) and sums them in
  * rank order on every rank, so T is bit-identical everywhere.
- * NCCL is loaded at run time (libnccl.so.2); O3G_ERR_COMM if unavailable. */
+ * NCCL is loaded at run time (libnccl.so.2); O3G_ERR_COMM if unavailable.
+ * world == 1 with a NULL id is the single-GPU path; world == 1 WITH an id
+ * creates a one-rank communicator and runs the distributed pass (rank slot,
+ * graph-captured ncclAllGather, rank-order tail) on one GPU — a self-test of
+ * the NCCL leg; results equal the single-GPU path's.                      */
 o3g_status o3g_nccl_unique_id(void* id_out_128);
 o3g_status o3g_dist_init(o3g_ctx* ctx, int rank, int world, const void* nccl_unique_id_128);
 

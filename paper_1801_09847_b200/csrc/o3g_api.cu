@@ -921,6 +921,8 @@ static o3g_status enqueue_pass(o3g_ctx* c, int blocks, bool write_corr, int32_t*
     if (c->estimation) tail_mode |= TAIL_P2P;
     // rank exchange through peer memory (o3g_dist_peer_connect / the loopback's
     // peer transport): K3's last block publishes to every rank, the tail waits
+    // (a world-1 communicator, o3g_dist_init's self-test form, runs the distributed pass too)
+    const bool distp = c->world > 1 || c->comm != nullptr;
     const bool peer = c->world > 1 && c->peer_xchg;
     Xchg* const* xp = peer ? c->xpeers.as<Xchg*>() : nullptr;
     const int xmode = peer ? TAIL_PEER : 0;
@@ -944,7 +946,7 @@ static o3g_status enqueue_pass(o3g_ctx* c, int blocks, bool write_corr, int32_t*
             ka.part_total = sblocks + blocks;
         }
         if (fused) {
-            ka.fuse_mode = c->world > 1 ? (TAIL_WRITE_RANK | xmode) : tail_mode;
+            ka.fuse_mode = distp ? (TAIL_WRITE_RANK | xmode) : tail_mode;
             ka.gathered = c->gathered.as<double>();
             ka.rank = c->rank;
             ka.xpeers = xp;
@@ -963,9 +965,9 @@ static o3g_status enqueue_pass(o3g_ctx* c, int blocks, bool write_corr, int32_t*
     const int nb = c->n_local > 0 ? blocks + (cert && c->cert_sweep ? sblocks : 0) : 0;
     double* gat = c->gathered.as<double>();
     IcpState* st = c->state.as<IcpState>();
-    if (fused && c->world == 1) {
+    if (fused && !distp) {
         // A6/A8 ran in the last K3 block
-    } else if (c->world == 1) {
+    } else if (!distp) {
         launch_tail(c->partials.as<double>(), nb, gat, 1, 0, st, hist, TAIL_REDUCE_BLOCKS | tail_mode, c->exec);
         ++*nlaunch;
     } else {
@@ -1290,7 +1292,9 @@ o3g_status o3g_dist_init(o3g_ctx* c, int rank, int world, const void* id) {
     c->comm = nullptr;
     c->rank = rank;
     c->world = world;
-    if (world == 1) return O3G_OK;
+    // world 1 with an id: a one-rank communicator (self-test of the NCCL leg on a
+    // single GPU: every pass then runs K3 -> rank slot -> ncclAllGather -> rank-order tail)
+    if (world == 1 && !id) return O3G_OK;
     if (!nccl().loaded) return fail(O3G_ERR_COMM, "libnccl.so.2 not loadable");
     nccl_uid uid;
     memcpy(&uid, id, sizeof(uid));

@@ -712,6 +712,41 @@ def test_loopback_multi_rank(o3g, workloads, world, transport):
                 c.close()
 
 
+def test_nccl_leg_one_rank(o3g, workloads):
+    """The NCCL leg of A7 on one GPU: o3g_dist_init(rank 0, world 1, id) creates
+    a one-rank communicator, and every pass then runs the distributed sequence
+    — K3's last block writes the rank slot, the graph-captured ncclAllGather,
+    the rank-order tail — instead of the fused single-GPU tail. Step terms,
+    the loop's T, fitness and rmse equal the single-GPU path's bit for bit
+    (one slot, same summation order), and the loop matches the oracle."""
+    w = workloads("depth")
+    T0 = w["init_T"]
+    try:
+        uid = o3g.nccl_unique_id()
+    except o3g.O3GError as e:   # (no libnccl.so.2 in this environment)
+        pytest.skip(f"NCCL not loadable: {e}")
+    ref = oracle.icp(w["source"], w["target"], w["target_normals"], w["dmax"], w["iters"], init_T=T0)
+    res = {}
+    for mode in ("single", "nccl"):
+        with o3g.Context(0) as ctx:
+            ctx.set_target(_dev(w["target"]), _dev(w["target_normals"]), w["dmax"])
+            if mode == "nccl":
+                ctx.dist_init(0, 1, uid)
+            ctx.set_source(_dev(w["source"]), T0)
+            corr = torch.empty(len(w["source"]), dtype=torch.int32, device="cuda")
+            st = ctx.step(T0, corr_out=corr)
+            l0 = ctx.launch_count()
+            r = ctx.run(T0, w["iters"])
+            res[mode] = (st["terms"].copy(), corr.cpu().numpy(), r, ctx.launch_count() - l0)
+    (t1, c1, r1, n1), (t2, c2, r2, n2) = res["single"], res["nccl"]
+    assert np.array_equal(t1, t2) and np.array_equal(c1, c2)
+    assert np.array_equal(r1.transformation, r2.transformation)
+    assert r1.fitness == r2.fitness and r1.inlier_rmse == r2.inlier_rmse and r1.iterations == r2.iterations
+    assert n2 > n1                      # (the distributed pass adds the rank-order tail launch)
+    assert np.abs(r2.transformation - ref["T"]).max() <= 1e-6
+    assert abs(r2.fitness - ref["fitness"]) <= 1e-6 and abs(r2.inlier_rmse - ref["inlier_rmse"]) <= 1e-6
+
+
 def test_certificate_tags_wrap(o3g, workloads):
     """Certificate records carry a 16-bit pass tag that advances across runs;
     records of an earlier run are older than any usable age, and the records

@@ -577,7 +577,7 @@ __device__ __forceinline__ bool cert_settle(const K3Args& a, const GridDev& g, c
 // instantiations every pass; the one that does not match the pass's mode
 // (IcpState::cmode, set on the device by the previous pass) exits at once.
 template <bool WRITE_CORR, bool COOP, bool PRUNE, bool CERT>
-__global__ void __launch_bounds__(kK3Threads, 4) k3_balanced(const K3Args a) {
+__global__ void __launch_bounds__(kK3Threads, 1024 / kK3Threads) k3_balanced(const K3Args a) {
     extern __shared__ __align__(16) unsigned char k3smem[];
     __shared__ double sT[12];
     __shared__ __align__(16) float4 sDT[CERT ? kCertAges : 1][3];   // (certificates: cert_tables)

@@ -13,7 +13,10 @@ constexpr int kTermStride = 32;   // padded per-block / per-rank partial
 // [29] queries that ran the full search, [30] candidates they scanned, [31]
 // queries settled by a valid certificate (k3_sweep)
 constexpr int kStatSearched = 29, kStatCandidates = 30, kStatCertified = 31, kTermsStats = 32;
-constexpr int kK3Threads = 256;   // correspondence kernel block size
+#ifndef O3G_K3_THREADS
+#define O3G_K3_THREADS 256
+#endif
+constexpr int kK3Threads = O3G_K3_THREADS;   // correspondence kernel block size
 constexpr int kTailThreads = 1024;
 
 // Voxel-hash grid over the target. Cell size

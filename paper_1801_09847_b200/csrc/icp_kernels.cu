@@ -174,7 +174,7 @@ __host__ __device__ inline size_t k3v2_warp_bytes(int hashed) {
     const size_t a = 32 * k3v2_slots(hashed) * sizeof(int2), b = 9 * kVW * sizeof(double);
     return a > b ? a : b;
 }
-inline size_t k3v2_smem(int hashed) { return (size_t)(kK3Threads / 32) * k3v2_warp_bytes(hashed); }
+inline size_t k3v2_smem(int hashed, int nt) { return (size_t)(nt / 32) * k3v2_warp_bytes(hashed); }
 
 // Row pruning, dense grid, light queries: the lane scans
 // the first non-empty x-row of its stencil (own row, faces, corners) first,
@@ -576,8 +576,8 @@ __device__ __forceinline__ bool cert_settle(const K3Args& a, const GridDev& g, c
 // every search leaves a certificate). A run with certificates launches both
 // instantiations every pass; the one that does not match the pass's mode
 // (IcpState::cmode, set on the device by the previous pass) exits at once.
-template <bool WRITE_CORR, bool COOP, bool PRUNE, bool CERT>
-__global__ void __launch_bounds__(kK3Threads, 1024 / kK3Threads) k3_balanced(const K3Args a) {
+template <bool WRITE_CORR, bool COOP, bool PRUNE, bool CERT, int NT>
+__global__ void __launch_bounds__(NT, 1024 / NT) k3_balanced(const K3Args a) {
     extern __shared__ __align__(16) unsigned char k3smem[];
     __shared__ double sT[12];
     __shared__ __align__(16) float4 sDT[CERT ? kCertAges : 1][3];   // (certificates: cert_tables)
@@ -606,15 +606,15 @@ __global__ void __launch_bounds__(kK3Threads, 1024 / kK3Threads) k3_balanced(con
     double acc0 = 0.0, acc1 = 0.0;           // C[lane>>2][2(lane&3)+{0,1}]
     const double r2 = a.r2;
 
-    const int gw = blockIdx.x * (kK3Threads / 32) + warp;
-    const int nw = gridDim.x * (kK3Threads / 32);
+    const int gw = blockIdx.x * (NT / 32) + warp;
+    const int nw = gridDim.x * (NT / 32);
     const int* __restrict__ cs = a.cell_start;
     const int nxny = g.nx * g.ny;
     // Live-query queue (dense grid with the occupancy bitmap): a first cheap
     // pass per batch of 32 (s' = T s, cell, one bitmap bit) drops queries
     // whose 27-cell stencil is empty; the rest are queued per warp and the
     // full search runs on full warps of live queries only.
-    __shared__ int qbuf[kK3Threads / 32][96];   // (< 32 queued + up to two batches)
+    __shared__ int qbuf[NT / 32][96];   // (< 32 queued + up to two batches)
     // the live-query pre-pass pays while many queries have nothing in reach;
     // once the previous pass matched at least half of the source it is
     // skipped (measured: large16m queue 0.650 vs 0.733 ms at T_init (fitness
@@ -626,9 +626,9 @@ __global__ void __launch_bounds__(kK3Threads, 1024 / kK3Threads) k3_balanced(con
     const bool warm = a.prev_j && !a.eval_T && a.st->passes > 0;
     const float Lout = __fmul_rd(a.h_rd, 1.0f - 1.1920928955078125e-07f);   // stencil reach >= h (§5.1 margins)
     const float dmax_hi = __double2float_ru(a.dmax * (1.0 + 9.094947017729282e-13));
-    __shared__ float4 s_gap[PRUNE && COOP ? kK3Threads / 32 : 1][32];
-    __shared__ int s_rmask[PRUNE && COOP ? kK3Threads / 32 : 1][32];
-    __shared__ float s_uw[PRUNE && COOP ? kK3Threads / 32 : 1][32];   // warm bound per query
+    __shared__ float4 s_gap[PRUNE && COOP ? NT / 32 : 1][32];
+    __shared__ int s_rmask[PRUNE && COOP ? NT / 32 : 1][32];
+    __shared__ float s_uw[PRUNE && COOP ? NT / 32 : 1][32];   // warm bound per query
     int qn = 0;   // warp-uniform queue length
     // flag mode (after k3_sweep): the warp walks chunks of kChunk consecutive
     // queries (chunk gw, gw + nw, ...), so its queue holds spatially close queries
@@ -645,7 +645,7 @@ __global__ void __launch_bounds__(kK3Threads, 1024 / kK3Threads) k3_balanced(con
     }
     int nsearch = 0, ncand = 0;   // this lane's full searches and their candidates (statistics)
     int ncert = 0;                // (fused certificate pass) queries settled by a certificate
-    __shared__ int s_stat[kK3Threads / 32][3];
+    __shared__ int s_stat[NT / 32][3];
     for (;;) {
         int i;
         if (use_queue) {
@@ -1330,10 +1330,10 @@ __global__ void __launch_bounds__(kK3Threads, 1024 / kK3Threads) k3_balanced(con
         const int ci = a.p2p ? term_cidx_p2p(threadIdx.x)
                              : (threadIdx.x < kTerms ? term_cidx(threadIdx.x) : -1);
         if (ci >= 0)
-            for (int w = 0; w < kK3Threads / 32; ++w)
+            for (int w = 0; w < NT / 32; ++w)
                 s += ((const double*)(k3smem + (size_t)w * k3v2_warp_bytes(g.hashed)))[ci];
         if (threadIdx.x == kStatSearched || threadIdx.x == kStatCandidates || (CERT && threadIdx.x == kStatCertified))
-            for (int w = 0; w < kK3Threads / 32; ++w) s += (double)s_stat[w][threadIdx.x - kStatSearched];
+            for (int w = 0; w < NT / 32; ++w) s += (double)s_stat[w][threadIdx.x - kStatSearched];
         a.block_partials[((size_t)blockIdx.y * gridDim.x + a.part_off + blockIdx.x) * kTermStride + threadIdx.x] = s;
     }
     if (!a.fuse_mode) return;
@@ -1354,7 +1354,7 @@ __global__ void __launch_bounds__(kK3Threads, 1024 / kK3Threads) k3_balanced(con
     // warp order; every load is a coalesced 256-byte partial row)
     {
         double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-        constexpr int W = kK3Threads / 32;
+        constexpr int W = NT / 32;
         int b = warp;
         for (; b + 3 * W < a.part_total; b += 4 * W) {
             s0 += __ldcg(&a.block_partials[(size_t)b * kTermStride + lane]);
@@ -1368,7 +1368,7 @@ __global__ void __launch_bounds__(kK3Threads, 1024 / kK3Threads) k3_balanced(con
     __syncthreads();
     if (threadIdx.x < kTermsStats) {
         double s = 0.0;
-        for (int w = 0; w < kK3Threads / 32; ++w)
+        for (int w = 0; w < NT / 32; ++w)
             s += ((const double*)(k3smem + (size_t)w * k3v2_warp_bytes(g.hashed)))[threadIdx.x];
         terms[threadIdx.x] = s;
     }
@@ -1556,47 +1556,62 @@ static int occ_of() {
     return b;
 }
 
-template <bool W, bool CO, bool PR, bool CE>
+template <bool W, bool CO, bool PR, bool CE, int NT>
 static int occ_v2(int hashed) {
     static bool attr_done = false;
     if (!attr_done) {
-        cudaFuncSetAttribute(k3_balanced<W, CO, PR, CE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)k3v2_smem(1));
+        cudaFuncSetAttribute(k3_balanced<W, CO, PR, CE, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)k3v2_smem(1, NT));
         attr_done = true;
     }
     int b = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k3_balanced<W, CO, PR, CE>, kK3Threads, k3v2_smem(hashed));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k3_balanced<W, CO, PR, CE, NT>, NT, k3v2_smem(hashed, NT));
     return b;
 }
 
-int k3_max_blocks_per_sm(int variant, bool write_corr, int hashed, bool prune) {
+template <int NT>
+static int occ_v2_nt(bool write_corr, int hashed, bool prune) {
+    // the cooperative / certificate instantiations have the same footprint class
+    if (prune) return write_corr ? occ_v2<true, false, true, false, NT>(hashed) : occ_v2<false, false, true, false, NT>(hashed);
+    return write_corr ? occ_v2<true, false, false, false, NT>(hashed) : occ_v2<false, false, false, false, NT>(hashed);
+}
+
+int k3_max_blocks_per_sm(int variant, bool write_corr, int hashed, bool prune, int nt) {
     switch (variant) {
         case 0: return write_corr ? occ_of<false, true>() : occ_of<false, false>();
         case 2: return write_corr ? occ_of<true, true>() : occ_of<true, false>();
         case 3: return k3_sorted_blocks_per_sm(write_corr, hashed);
         case 4: return k3_tiled_blocks_per_sm(write_corr);
-        default:   // the cooperative / certificate instantiations have the same footprint class
-            if (prune) return write_corr ? occ_v2<true, false, true, false>(hashed) : occ_v2<false, false, true, false>(hashed);
-            return write_corr ? occ_v2<true, false, false, false>(hashed) : occ_v2<false, false, false, false>(hashed);
+        default:
+            return nt == 1024 ? occ_v2_nt<1024>(write_corr, hashed, prune)
+                 : nt == 512  ? occ_v2_nt<512>(write_corr, hashed, prune)
+                              : occ_v2_nt<256>(write_corr, hashed, prune);
     }
 }
 
-template <bool CE>
-static void launch_balanced(const K3Args& a, int sel, dim3 grid, size_t sm, cudaStream_t s) {
-    occ_v2<true, false, false, CE>(a.g.hashed), occ_v2<false, false, false, CE>(a.g.hashed);
-    occ_v2<true, true, false, CE>(a.g.hashed), occ_v2<false, true, false, CE>(a.g.hashed);
-    occ_v2<true, false, true, CE>(a.g.hashed), occ_v2<false, false, true, CE>(a.g.hashed);
-    occ_v2<true, true, true, CE>(a.g.hashed), occ_v2<false, true, true, CE>(a.g.hashed);
+template <bool CE, int NT>
+static void launch_balanced(const K3Args& a, int sel, dim3 grid, cudaStream_t s) {
+    const size_t sm = k3v2_smem(a.g.hashed, NT);
+    occ_v2<true, false, false, CE, NT>(a.g.hashed), occ_v2<false, false, false, CE, NT>(a.g.hashed);
+    occ_v2<true, true, false, CE, NT>(a.g.hashed), occ_v2<false, true, false, CE, NT>(a.g.hashed);
+    occ_v2<true, false, true, CE, NT>(a.g.hashed), occ_v2<false, false, true, CE, NT>(a.g.hashed);
+    occ_v2<true, true, true, CE, NT>(a.g.hashed), occ_v2<false, true, true, CE, NT>(a.g.hashed);
     switch (sel) {
-        case 0: k3_balanced<false, false, false, CE><<<grid, kK3Threads, sm, s>>>(a); break;
-        case 1: k3_balanced<false, false, true, CE><<<grid, kK3Threads, sm, s>>>(a); break;
-        case 2: k3_balanced<false, true, false, CE><<<grid, kK3Threads, sm, s>>>(a); break;
-        case 3: k3_balanced<false, true, true, CE><<<grid, kK3Threads, sm, s>>>(a); break;
-        case 4: k3_balanced<true, false, false, CE><<<grid, kK3Threads, sm, s>>>(a); break;
-        case 5: k3_balanced<true, false, true, CE><<<grid, kK3Threads, sm, s>>>(a); break;
-        case 6: k3_balanced<true, true, false, CE><<<grid, kK3Threads, sm, s>>>(a); break;
-        default: k3_balanced<true, true, true, CE><<<grid, kK3Threads, sm, s>>>(a); break;
+        case 0: k3_balanced<false, false, false, CE, NT><<<grid, NT, sm, s>>>(a); break;
+        case 1: k3_balanced<false, false, true, CE, NT><<<grid, NT, sm, s>>>(a); break;
+        case 2: k3_balanced<false, true, false, CE, NT><<<grid, NT, sm, s>>>(a); break;
+        case 3: k3_balanced<false, true, true, CE, NT><<<grid, NT, sm, s>>>(a); break;
+        case 4: k3_balanced<true, false, false, CE, NT><<<grid, NT, sm, s>>>(a); break;
+        case 5: k3_balanced<true, false, true, CE, NT><<<grid, NT, sm, s>>>(a); break;
+        case 6: k3_balanced<true, true, false, CE, NT><<<grid, NT, sm, s>>>(a); break;
+        default: k3_balanced<true, true, true, CE, NT><<<grid, NT, sm, s>>>(a); break;
     }
+}
+template <bool CE>
+static void launch_balanced_nt(const K3Args& a, int sel, dim3 grid, cudaStream_t s) {
+    if (a.nt == 1024) launch_balanced<CE, 1024>(a, sel, grid, s);
+    else if (a.nt == 512) launch_balanced<CE, 512>(a, sel, grid, s);
+    else launch_balanced<CE, 256>(a, sel, grid, s);
 }
 
 // variant 1 with certificates (a.cert set): both search instantiations are
@@ -1615,11 +1630,10 @@ void launch_k3(const K3Args& a, int blocks, int variant, bool write_corr, cudaSt
         case 3: launch_k3_sorted(a, blocks, write_corr, s); break;
         case 4: launch_k3_tiled(a, blocks, write_corr, s); break;
         default: {
-            const size_t sm = k3v2_smem(a.g.hashed);
             const dim3 grid(blocks, a.eval_T ? a.n_eval : 1);
             const int sel = (write_corr ? 4 : 0) | (a.coop_min > 0 ? 2 : 0) | (a.prune ? 1 : 0);
-            launch_balanced<false>(a, sel, grid, sm, s);
-            if (a.cert && !a.eval_T) launch_balanced<true>(a, sel, grid, sm, s);
+            launch_balanced_nt<false>(a, sel, grid, s);
+            if (a.cert && !a.eval_T) launch_balanced_nt<true>(a, sel, grid, s);
         }
     }
 }

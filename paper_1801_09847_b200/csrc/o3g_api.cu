@@ -825,9 +825,10 @@ static int k3_variant(const o3g_ctx* c) {
 }
 
 static int k3_blocks(o3g_ctx* c, bool write_corr) {
-    int bps = c->bps_override ? c->bps_override : k3_max_blocks_per_sm(k3_variant(c), write_corr, c->g.hashed, prune_of(c) >= 0);
+    const int nt = k3_balanced_threads(c->n_local);
+    int bps = c->bps_override ? c->bps_override : k3_max_blocks_per_sm(k3_variant(c), write_corr, c->g.hashed, prune_of(c) >= 0, nt);
     if (bps < 1) bps = 1;
-    const int tpb = k3_threads(k3_variant(c));
+    const int tpb = k3_threads(k3_variant(c), nt);
     int64_t need = (c->n_local + tpb - 1) / tpb;
     int64_t b = (int64_t)c->sms * bps;
     if (need < b) b = need;
@@ -872,6 +873,7 @@ static K3Args k3_args(o3g_ctx* c, int32_t* corr) {
     const bool ilv = c->interleave == 1 || (c->interleave == -1 && coop_min_of(c) > 0);
     a.ilv = ilv ? (int)((c->n_local + 31) / 32) : 0;
     a.xsorted = c->xsorted ? 1 : 0;
+    a.nt = k3_balanced_threads(c->n_local);
     a.prev_j = nullptr;   // (set by the run loop: o3g_icp_run)
     a.cert = nullptr;     // (idem)
     a.need = nullptr;

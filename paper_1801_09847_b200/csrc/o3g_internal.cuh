@@ -241,6 +241,7 @@ struct K3Args {
     // (this rank's own buffer at [rank]; a device array of world pointers)
     Xchg* const* xpeers;
     int world;
+    int nt;   // variant 1: threads per block (256, 512 or 1024; k3_balanced_threads)
 };
 constexpr int kCertAges = 32;     // certificates older than this many passes expire
 // variant: 0 = exact fp64 scan (k3_corr_reduce), 1 = two-pass warp kernel
@@ -248,7 +249,11 @@ constexpr int kCertAges = 32;     // certificates older than this many passes ex
 // 3 = tile-sorted two-pass kernel (k3_sorted), 4 = smem-staged tiles (k3_tiled).
 // Identical correspondences.
 constexpr int kTileQ = 128;       // variant 4: queries per tile (max)
-inline int k3_threads(int variant) { return variant == 3 ? 128 : variant == 4 ? kTileQ : kK3Threads; }
+// variant 1's block size (K3Args::nt): 1024 threads (one block per SM) for shards of
+// >= 2^19 queries, 512 below (measured: large16m K3 0.601 ms at 256, 0.593 at 512,
+// 0.559 at 1024; depth 0.038 / 0.036 / 0.044; profiles/r02_cert_modes.txt)
+inline int k3_balanced_threads(int64_t n_local) { return n_local >= (1 << 19) ? 1024 : 512; }
+inline int k3_threads(int variant, int nt) { return variant == 3 ? 128 : variant == 4 ? kTileQ : variant == 1 ? nt : kK3Threads; }
 int k3_tiled_blocks_per_sm(bool write_corr);
 void launch_k3_tiled(const K3Args& a, int blocks, bool write_corr, cudaStream_t s);
 int k3_sorted_blocks_per_sm(bool write_corr, int hashed);
@@ -256,7 +261,7 @@ void launch_k3_sorted(const K3Args& a, int blocks, bool write_corr, cudaStream_t
 void launch_k3(const K3Args& a, int blocks, int variant, bool write_corr, cudaStream_t s);
 int k3_sweep_blocks_per_sm();
 void launch_k3_sweep(const K3Args& a, int blocks, bool write_corr, cudaStream_t s);
-int k3_max_blocks_per_sm(int variant, bool write_corr, int hashed, bool prune);
+int k3_max_blocks_per_sm(int variant, bool write_corr, int hashed, bool prune, int nt);
 void launch_eval_reduce(const double* partials, int nblocks, int k, double n_total, double* fit,
                         double* rmse, cudaStream_t s);
 struct TailHist {

@@ -8,6 +8,7 @@ import argparse
 import csv
 import json
 import os
+import re
 
 ap = argparse.ArgumentParser()
 ap.add_argument("csv")
@@ -30,7 +31,11 @@ passes, cur = [], None
 # plain one, then the certificate one; the one not matching the pass's mode
 # exits at once), after k3_sweep in sweep mode: a pass ends at the certificate
 # instantiation; without certificates at each k3_balanced
-certs = any(L["name"].replace(" ", "").rstrip().split("(")[0].endswith(",1>") for L in launches.values())
+def is_cert(name):   # k3_balanced<WRITE_CORR, COOP, PRUNE, CERT, NT>: the certificate instantiation
+    return re.search(r"k3_balanced<(\(bool\))?\d,(\(bool\))?\d,(\(bool\))?\d,(\(bool\))?1[,>]", name.replace(" ", "")) is not None
+
+
+certs = any(is_cert(L["name"]) for L in launches.values())
 for i in sorted(launches):
     L = launches[i]
     t, tu = L["gpu__time_duration.sum"]
@@ -40,7 +45,7 @@ for i in sorted(launches):
         return v * {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3}.get(u, 1e-6)
     rec = (t, mb("dram__bytes_read.sum") + mb("dram__bytes_write.sum"))
     cur = (rec[0] + (cur[0] if cur else 0.0), rec[1] + (cur[1] if cur else 0.0))
-    ends = "k3_balanced" in L["name"] and (not certs or L["name"].replace(" ", "").rstrip().split("(")[0].endswith(",1>"))
+    ends = "k3_balanced" in L["name"] and (not certs or is_cert(L["name"]))
     if ends:
         passes.append(cur)
         cur = None

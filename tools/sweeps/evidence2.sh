@@ -14,6 +14,6 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpuru
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${T}_launches_conv.csv python tools/profile_run.py --reps 1 --regime converged > /dev/null 2>&1; echo ncu2 rc=$?
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:k3_ --csv --log-file gpurun_out/${T}_traffic_init.csv python tools/profile_run.py --reps 1 > /dev/null 2>&1; echo ncu3 rc=$?
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:k3_ --csv --log-file gpurun_out/${T}_traffic_conv.csv python tools/profile_run.py --reps 1 --regime converged > /dev/null 2>&1; echo ncu4 rc=$?
-ncu --set full --import-source on --clock-control none --kernel-name-base demangled -k "regex:k3_balanced<.bool.0, .bool.0, .bool.0, .bool.0>" -s 5 -c 1 -o gpurun_out/${T}_k3_init python tools/profile_run.py > /dev/null 2>&1; echo ncu5 rc=$?
-ncu --set full --import-source on --clock-control none --kernel-name-base demangled -k "regex:k3_balanced<.bool.0, .bool.0, .bool.0, .bool.1>" -s 12 -c 1 -o gpurun_out/${T}_k3_conv python tools/profile_run.py --regime converged > /dev/null 2>&1; echo ncu6 rc=$?
+ncu --set full --import-source on --clock-control none --kernel-name-base demangled -k "regex:k3_balanced<.bool.0, .bool.0, .bool.0, .bool.0," -s 5 -c 1 -o gpurun_out/${T}_k3_init python tools/profile_run.py > /dev/null 2>&1; echo ncu5 rc=$?
+ncu --set full --import-source on --clock-control none --kernel-name-base demangled -k "regex:k3_balanced<.bool.0, .bool.0, .bool.0, .bool.1," -s 12 -c 1 -o gpurun_out/${T}_k3_conv python tools/profile_run.py --regime converged > /dev/null 2>&1; echo ncu6 rc=$?
 ncu --set full --import-source on --clock-control none -k regex:k3_balanced -s 20 -c 1 -o gpurun_out/${T}_k3_lidar python tools/profile_run.py --config lidar > /dev/null 2>&1; echo ncu7 rc=$?

@@ -305,8 +305,7 @@ def main():
             r = ctx.run_multiscale(s_, t_, n_, vox, dms, its, init=T0, relative_fitness=0.0,
                                    relative_rmse=0.0)
             return int(np.sum(r["n_source"] * r["iterations"])), r
-        ctx.set_target(t_, n_, w["dmax"])
-        ctx.set_source(s_, T0)
+        ctx.set_clouds(s_, t_, n_, w["dmax"], T0)   # (A1 + A2; sequential inside when distributed)
         r = ctx.run(T0, iters, 0.0, 0.0)
         return n * r.iterations, r
 
@@ -358,8 +357,7 @@ def main():
     # settled by a certificate, mean candidates per search
     passes = None
     if not multiscale:
-        ctx.set_target(tgt, nrm, w["dmax"])
-        ctx.set_source(src, T0)
+        ctx.set_clouds(src, tgt, nrm, w["dmax"], T0)
         rh = ctx.run(T0, iters, 0.0, 0.0, history=True)
         tr = ctx.last_run_trace(rh.passes)
         passes = [{"fitness": round(float(f), 6), "inliers": int(tr["terms"][k][27]),
@@ -384,8 +382,7 @@ def main():
                 units2, r2 = step(src, tgt, nrm)
                 e1.record()
             else:
-                ctx.set_target(tgt, nrm, w["dmax"])
-                ctx.set_source(src, T_start)
+                ctx.set_clouds(src, tgt, nrm, w["dmax"], T_start)
                 e0.record()
                 r2 = ctx.run(T_start, iters, 0.0, 0.0)
                 e1.record()
@@ -409,8 +406,7 @@ def main():
                 scratch.fill_(1)
             e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
             e[0].record()
-            ctx.set_target(tgt, nrm, w["dmax"])
-            ctx.set_source(src, T0)
+            ctx.set_clouds(src, tgt, nrm, w["dmax"], T0)
             e[1].record()
             ctx.run(T0, iters, 0.0, 0.0)
             e[2].record()

@@ -131,6 +131,18 @@ o3g_status o3g_set_target(o3g_ctx* ctx, const float* xyz, const float* normals, 
  * must live on the context's device (O3G_ERR_INVALID_ARGUMENT otherwise). */
 o3g_status o3g_set_source(o3g_ctx* ctx, const float* xyz, int64_t n, const double order_T[16]);
 
+/* A1 + A2 in one call: o3g_set_target(target_xyz, target_normals, n_target,
+ * dmax) followed by o3g_set_source(source_xyz, n_source, order_T), same
+ * arguments, results and errors (this is what o3g_icp_point_to_plane does
+ * with its clouds). With device-resident arrays on a single GPU the source's
+ * bbox, ordering keys, sort and gather only need the grid's dimensions, so
+ * they run on a second stream with their own scratch beside the target's
+ * sort, cell table, gather and bitmaps, and the call waits once for both;
+ * host arrays are staged with their copies overlapped with the build.      */
+o3g_status o3g_set_clouds(o3g_ctx* ctx, const float* source_xyz, int64_t n_source,
+                          const float* target_xyz, const float* target_normals, int64_t n_target,
+                          double max_correspondence_distance, const double order_T[16]);
+
 /* One correspondence + reduction pass at fixed T_in (north_star's
  * o3g_icp_step). Outputs:
  *   corr_out: DEVICE int32 [n] or NULL. Written in ORIGINAL source order

@@ -189,6 +189,12 @@ struct o3g_ctx {
     int rank = 0, world = 1;
     bool loopback = false;         // o3g_dist_init_loopback: no communicator (o3g_loopback_run)
     nccl_comm_t comm = nullptr;
+    // o3g_set_clouds: the source's keys / sort / gather run on a side stream beside the
+    // target build, on their own scratch
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_side = nullptr;
+    DevBuf s_keys_a, s_keys_b, s_vals_a, s_vals_b, s_cub;
+    int64_t pend_src_n = 0, pend_src_lo = 0, pend_src_hi = 0;   // set_source results awaiting source_finish
     // peer-memory exchange (o3g_dist_peer_*): this rank's Xchg, the device array of
     // every rank's Xchg pointer, and the peers' buffers opened through CUDA IPC
     DevBuf xchg, xpeers;
@@ -371,6 +377,9 @@ o3g_status o3g_destroy(o3g_ctx* c) {
     if (c->comm && nccl().comm_destroy) nccl().comm_destroy(c->comm);
     peer_disconnect(c);
     c->xchg.release();
+    for (DevBuf* b : {&c->s_keys_a, &c->s_keys_b, &c->s_vals_a, &c->s_vals_b, &c->s_cub}) b->release();
+    if (c->ev_side) cudaEventDestroy(c->ev_side);
+    if (c->side) cudaStreamDestroy(c->side);
     if (c->h_state) cudaFreeHost(c->h_state);
     if (c->fence) cudaEventDestroy(c->fence);
     for (cudaEvent_t e : c->ev_copy)
@@ -446,8 +455,12 @@ o3g_status o3g_set_option(o3g_ctx* c, int option, int64_t value) {
 
 // normals_ready (nullable): the normals arrive later on another stream; the
 // gather waits for it and their finiteness is checked at the final sync
+static o3g_status target_finish(o3g_ctx* c, bool normals_late);
+
+// defer_final: return once everything is enqueued (the grid parameters are known and
+// stored); the caller runs target_finish after its own work (o3g_set_clouds)
 static o3g_status set_target_impl(o3g_ctx* c, const float* xyz, const float* normals, int64_t n,
-                                  double dmax, cudaEvent_t normals_ready) {
+                                  double dmax, cudaEvent_t normals_ready, bool defer_final = false) {
     if (!c) return fail(O3G_ERR_INVALID_ARGUMENT, "ctx is NULL");
     if (!xyz) return fail(O3G_ERR_INVALID_ARGUMENT, "target xyz is required");
     if (n <= 0 || n > 0x7ffffffeLL) return fail(O3G_ERR_INVALID_ARGUMENT, "n_target must be in [1, 2^31-2]");
@@ -599,17 +612,32 @@ static o3g_status set_target_impl(o3g_ctx* c, const float* xyz, const float* nor
         c->launches += 4;
         c->nbr_ready = true;
     }
-    unsigned long long h_occ = 0;
-    int32_t h_bad2 = 0;
-    CK(cudaMemcpyAsync(&h_occ, occ, 8, cudaMemcpyDeviceToHost, c->exec));
-    if (normals_ready) CK(cudaMemcpyAsync(&h_bad2, bad, 4, cudaMemcpyDeviceToHost, c->exec));
-    CK(cudaStreamSynchronize(c->exec));
-    CK(cudaGetLastError());
-    if (h_bad2) return fail(O3G_ERR_INVALID_ARGUMENT, "non-finite target coordinate or normal");
     c->g = g;
     c->m = n;
     c->dmax = dmax;
     c->has_normals = dn != nullptr;
+    c->xsorted = false;
+    if (defer_final) return O3G_OK;
+    return target_finish(c, normals_ready != nullptr);
+}
+
+// the end of o3g_set_target: wait for the build, read the occupied-cell count (and the
+// late normals' finiteness flag), then the x-order inside cells for dense targets
+static o3g_status target_finish(o3g_ctx* c, bool normals_late) {
+    const GridDev g = c->g;
+    const int64_t n = c->m;
+    uint32_t* mm = c->misc.as<uint32_t>();
+    int32_t* bad = (int32_t*)(mm + 6);
+    unsigned long long* occ = (unsigned long long*)(mm + 8);
+    unsigned long long h_occ = 0;
+    int32_t h_bad2 = 0;
+    c->m = 0;   // (until the build is known to be good)
+    CK(cudaMemcpyAsync(&h_occ, occ, 8, cudaMemcpyDeviceToHost, c->exec));
+    if (normals_late) CK(cudaMemcpyAsync(&h_bad2, bad, 4, cudaMemcpyDeviceToHost, c->exec));
+    CK(cudaStreamSynchronize(c->exec));
+    CK(cudaGetLastError());
+    if (h_bad2) return fail(O3G_ERR_INVALID_ARGUMENT, "non-finite target coordinate or normal");
+    c->m = n;
     c->occupied = (int64_t)h_occ;
     // x-order inside cells for dense targets (the cooperative path's x-windows):
     // auto when the target averages >= 32 points per occupied cell
@@ -647,14 +675,18 @@ o3g_status o3g_set_target(o3g_ctx* c, const float* xyz, const float* normals, in
     return set_target_impl(c, xyz, normals, n, dmax, nullptr);
 }
 
-o3g_status o3g_set_source(o3g_ctx* c, const float* xyz, int64_t n, const double order_T[16]) {
+static o3g_status source_finish(o3g_ctx* c);
+
+// defer: enqueue only, on c->exec as the caller set it (no wait for the user stream, no
+// final sync); the caller runs source_finish afterwards (o3g_set_clouds)
+static o3g_status set_source_impl(o3g_ctx* c, const float* xyz, int64_t n, const double order_T[16], bool defer) {
     if (!c) return fail(O3G_ERR_INVALID_ARGUMENT, "ctx is NULL");
     if (!xyz) return fail(O3G_ERR_INVALID_ARGUMENT, "source xyz is required");
     // (the kernels' 32-bit batch cursors step by up to 2^24 past the last query)
     if (n <= 0 || n > 0x7effffffLL) return fail(O3G_ERR_INVALID_ARGUMENT, "n_source must be in [1, 2^31 - 2^24]");
     if (c->m <= 0) return fail(O3G_ERR_INVALID_ARGUMENT, "o3g_set_target must be called first");
     if (order_T && !rigid_ok(order_T)) return fail(O3G_ERR_INVALID_ARGUMENT, "order_T is not a rigid transform");
-    TRY(enter(c));
+    if (!defer) TRY(enter(c));
     c->src_ready = false;
     invalidate_graph(c);
     const float* dx;
@@ -780,6 +812,14 @@ o3g_status o3g_set_source(o3g_ctx* c, const float* xyz, int64_t n, const double 
         CK(cudaMemcpyAsync(&c->ntiles, nsel, 4, cudaMemcpyDeviceToHost, c->exec));
         c->launches += 5;
     }
+    c->pend_src_n = n, c->pend_src_lo = lo, c->pend_src_hi = hi;
+    if (defer) return O3G_OK;
+    return source_finish(c);
+}
+
+// the end of o3g_set_source: wait, read the finiteness flag and the source bbox
+static o3g_status source_finish(o3g_ctx* c) {
+    const uint32_t* smm = c->misc.as<uint32_t>() + 24;
     int32_t h_bad = 0;
     uint32_t h_mm[6];
     CK(cudaMemcpyAsync(&h_bad, (int32_t*)(c->misc.as<uint32_t>() + 6), 4, cudaMemcpyDeviceToHost, c->exec));
@@ -788,11 +828,15 @@ o3g_status o3g_set_source(o3g_ctx* c, const float* xyz, int64_t n, const double 
     CK(cudaGetLastError());
     if (h_bad) return fail(O3G_ERR_INVALID_ARGUMENT, "non-finite source coordinate");
     for (int a = 0; a < 3; ++a) c->smax[a] = fmaxf(fabsf(ord2f(h_mm[a])), fabsf(ord2f(h_mm[3 + a])));
-    c->n_total = n;
-    c->n_local = hi - lo;
-    c->shard_lo = lo;
+    c->n_total = c->pend_src_n;
+    c->n_local = c->pend_src_hi - c->pend_src_lo;
+    c->shard_lo = c->pend_src_lo;
     c->src_ready = true;
     return O3G_OK;
+}
+
+o3g_status o3g_set_source(o3g_ctx* c, const float* xyz, int64_t n, const double order_T[16]) {
+    return set_source_impl(c, xyz, n, order_T, false);
 }
 
 static int coop_min_of(const o3g_ctx* c) {
@@ -1744,6 +1788,46 @@ extern "C" o3g_status o3g_icp_multiscale(o3g_ctx* c, const float* src, int64_t n
 static o3g_status set_inputs(o3g_ctx* c, const float* src, int64_t ns, const float* tgt,
                              const float* nrm, int64_t nt, double dmax, const double order_T[16]) {
     const bool host = !is_device_ptr(src) && !is_device_ptr(tgt) && !(nrm && is_device_ptr(nrm));
+    // device-resident clouds on one GPU: the source's bbox / keys / sort / gather need
+    // only the grid's dimensions, so they run on a side stream (own scratch) beside the
+    // target's sort, cell table, gather and bitmaps; one final wait for both
+    const bool dev3 = src && tgt && is_device_ptr(src) && is_device_ptr(tgt) && (!nrm || is_device_ptr(nrm)) &&
+                      !foreign_device_ptr(src, c->device) && !foreign_device_ptr(tgt, c->device) &&
+                      !(nrm && foreign_device_ptr(nrm, c->device));
+    if (dev3 && c->world == 1 && c->search != 4 && c->target_sort == 1 && ns > 0 && nt > 0 &&
+        ns <= 0x7effffffLL && nt <= 0x7ffffffeLL && (!order_T || rigid_ok(order_T))) {
+        CK(cudaSetDevice(c->device));
+        if (!c->side) {
+            CK(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+            CK(cudaEventCreateWithFlags(&c->ev_side, cudaEventDisableTiming));
+        }
+        TRY(c->s_keys_a.ensure((size_t)ns * 4));
+        TRY(c->s_keys_b.ensure((size_t)ns * 4));
+        TRY(c->s_vals_a.ensure((size_t)ns * 4));
+        TRY(c->s_vals_b.ensure((size_t)ns * 4));
+        TRY(set_target_impl(c, tgt, nrm, nt, dmax, nullptr, /*defer_final=*/true));
+        // (the side stream starts from the caller's stream position, as exec did in enter())
+        CK(cudaStreamWaitEvent(c->side, c->fence, 0));
+        auto swap_scratch = [&]() {
+            std::swap(c->keys_a, c->s_keys_a), std::swap(c->keys_b, c->s_keys_b);
+            std::swap(c->vals_a, c->s_vals_a), std::swap(c->vals_b, c->s_vals_b);
+            std::swap(c->cub_tmp, c->s_cub), std::swap(c->exec, c->side);
+        };
+        swap_scratch();
+        o3g_status st = set_source_impl(c, src, ns, order_T, /*defer=*/true);
+        cudaError_t e = st == O3G_OK ? cudaEventRecord(c->ev_side, c->exec) : cudaSuccess;
+        swap_scratch();
+        if (st == O3G_OK && e == cudaSuccess) e = cudaStreamWaitEvent(c->exec, c->ev_side, 0);
+        if (st != O3G_OK || e != cudaSuccess) {
+            cudaStreamSynchronize(c->side);
+            cudaStreamSynchronize(c->exec);
+            c->m = 0;
+            if (st != O3G_OK) return st;
+            return fail(O3G_ERR_CUDA, cudaGetErrorString(e));
+        }
+        TRY(target_finish(c, false));
+        return source_finish(c);
+    }
     if (!host || ns <= 0 || nt <= 0 || ns > 0x7ffffffeLL || nt > 0x7ffffffeLL) {
         TRY(o3g_set_target(c, tgt, nrm, nt, dmax));
         return o3g_set_source(c, src, ns, order_T);
@@ -1771,6 +1855,14 @@ static o3g_status set_inputs(o3g_ctx* c, const float* src, int64_t ns, const flo
                         c->ev_copy[1]));
     CK(cudaStreamWaitEvent(c->exec, c->ev_copy[2], 0));
     return o3g_set_source(c, c->stage_c.as<float>(), ns, order_T);
+}
+
+o3g_status o3g_set_clouds(o3g_ctx* c, const float* source_xyz, int64_t n_source, const float* target_xyz,
+                          const float* target_normals, int64_t n_target, double dmax,
+                          const double order_T[16]) {
+    if (!c) return fail(O3G_ERR_INVALID_ARGUMENT, "ctx is NULL");
+    if (!source_xyz || !target_xyz) return fail(O3G_ERR_INVALID_ARGUMENT, "source and target xyz are required");
+    return set_inputs(c, source_xyz, n_source, target_xyz, target_normals, n_target, dmax, order_T);
 }
 
 o3g_status o3g_icp_point_to_point(const float* source_xyz, int64_t n_source, const float* target_xyz,

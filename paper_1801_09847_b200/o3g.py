@@ -69,6 +69,7 @@ def lib() -> C.CDLL:
             "o3g_icp_step": [P, P, P, P, P, P, P, P],
             "o3g_icp_run": [P, P, I32, D, D, P, P, P, P, P, P],
             "o3g_nccl_unique_id": [P],
+            "o3g_set_clouds": [P, P, I64, P, P, I64, D, P],
             "o3g_dist_init": [P, C.c_int, C.c_int, P],
             "o3g_dist_init_loopback": [P, C.c_int, C.c_int],
             "o3g_loopback_run": [P, C.c_int, P, I32, D, D, P, P, P, P],
@@ -272,6 +273,19 @@ class Context:
         keep: list = []
         p, n = _pts(xyz, "source", keep)
         _check(lib().o3g_set_source(self._h, p, n, _mat(order_T, keep)))
+        self.n_source = n
+
+    def set_clouds(self, source, target, target_normals, max_correspondence_distance, order_T=None):
+        """o3g_set_clouds: set_target + set_source in one call (device arrays: the
+        source's ordering runs beside the target build)."""
+        keep: list = []
+        ps, n = _pts(source, "source", keep)
+        pt, m = _pts(target, "target", keep)
+        pn, mn = _pts(target_normals, "target_normals", keep)
+        if pn is not None and mn != m:
+            raise InvalidArgument(ERR_INVALID_ARGUMENT, "target and normals must have the same count")
+        _check(lib().o3g_set_clouds(self._h, ps, n, pt, pn, m, float(max_correspondence_distance),
+                                    _mat(order_T, keep)))
         self.n_source = n
 
     def dist_init(self, rank: int, world: int, unique_id: bytes | None):

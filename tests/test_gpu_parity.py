@@ -712,6 +712,56 @@ def test_loopback_multi_rank(o3g, workloads, world, transport):
                 c.close()
 
 
+def test_set_clouds_matches_sequential(o3g, workloads):
+    """o3g_set_clouds (the source's ordering on a side stream beside the target
+    build) leaves exactly the state of o3g_set_target + o3g_set_source: step
+    correspondences and terms, and the loop's T, fitness and rmse are equal
+    bit for bit, on a sparse target (tiny), a pruning-instantiation target
+    (depth), an x-sorted dense target (lidar) and a 400k shard; repeated calls
+    on one context reuse the side scratch; non-finite input fails the call."""
+    cases = [("tiny", workloads("tiny")), ("depth", workloads("depth")), ("lidar", workloads("lidar")),
+             ("large400k", workloads("large16m", n=400_000))]
+    for name, w in cases:
+        T0 = w["init_T"]
+        n = len(w["source"])
+        s_, t_, n_ = _dev(w["source"]), _dev(w["target"]), _dev(w["target_normals"])
+        out = []
+        for mode in ("sequential", "clouds", "clouds"):
+            ctx = out[1][3] if mode == "clouds" and len(out) == 2 else o3g.Context(0)
+            if mode == "sequential":
+                ctx.set_target(t_, n_, w["dmax"])
+                ctx.set_source(s_, T0)
+            else:
+                ctx.set_clouds(s_, t_, n_, w["dmax"], T0)
+            corr = torch.empty(n, dtype=torch.int32, device="cuda")
+            st = ctx.step(T0, corr_out=corr)
+            r = ctx.run(T0, min(w["iters"], 8))
+            out.append((st["terms"].copy(), corr.cpu().numpy(), r, ctx, ctx.grid_info()))
+        a = out[0]
+        for b in out[1:]:
+            assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1]), name
+            assert np.array_equal(a[2].transformation, b[2].transformation), name
+            assert a[2].fitness == b[2].fitness and a[2].inlier_rmse == b[2].inlier_rmse, name
+            assert a[4] == b[4], name
+        out[0][3].close()
+        out[1][3].close()
+    w = workloads("tiny")
+    bad_s = w["source"].copy()
+    bad_s[17, 1] = np.nan
+    bad_t = w["target"].copy()
+    bad_t[5, 0] = np.inf
+    with o3g.Context(0) as ctx:
+        with pytest.raises(o3g.InvalidArgument):
+            ctx.set_clouds(_dev(bad_s), _dev(w["target"]), _dev(w["target_normals"]), w["dmax"])
+        with pytest.raises(o3g.InvalidArgument):
+            ctx.set_clouds(_dev(w["source"]), _dev(bad_t), _dev(w["target_normals"]), w["dmax"])
+        with pytest.raises(o3g.O3GError):
+            ctx.step(w["init_T"])                      # (nothing usable was set)
+        ctx.set_clouds(_dev(w["source"]), _dev(w["target"]), _dev(w["target_normals"]), w["dmax"])
+        ref = oracle.step(w["init_T"], w["source"], w["target"], w["target_normals"], w["dmax"])
+        _terms_ok(ctx.step(w["init_T"])["terms"], ref)
+
+
 def test_nccl_leg_one_rank(o3g, workloads):
     """The NCCL leg of A7 on one GPU: o3g_dist_init(rank 0, world 1, id) creates
     a one-rank communicator, and every pass then runs the distributed sequence

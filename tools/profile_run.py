@@ -50,8 +50,7 @@ if a.cert is not None:
 if a.interleave is not None:
     ctx.set_option(11, a.interleave)
 for _ in range(a.reps):
-    ctx.set_target(tgt, nrm, w["dmax"])
-    ctx.set_source(src, w["init_T"])
+    ctx.set_clouds(src, tgt, nrm, w["dmax"], w["init_T"])
     if a.mode == "run":
         r = ctx.run(w["init_T"], a.iters if a.iters is not None else w["iters"], 0.0, 0.0)
         print("fitness", r.fitness, "rmse", r.inlier_rmse, "iters", r.iterations)

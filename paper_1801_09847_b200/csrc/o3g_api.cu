@@ -2,6 +2,7 @@
 // context (device buffers, grid build, source ordering), the graph-launched
 // iteration loop and the multi-GPU exchange (NCCL, loaded at run time).
 #include <dlfcn.h>
+#include <nvtx3/nvToolsExt.h>   // header-only; a no-op unless a profiler injects itself
 #include <stdio.h>
 #include <stdlib.h>
 #include <math.h>
@@ -45,6 +46,18 @@ static o3g_status fail(o3g_status s, const std::string& msg) {
     } while (0)
 
 // --------------------------------------------------------- device buffers
+// NVTX phase ranges: one range per API phase on the calling thread
+struct PhaseRange {
+#ifndef O3G_NO_NVTX
+    explicit PhaseRange(const char* name) { nvtxRangePushA(name); }
+    ~PhaseRange() { nvtxRangePop(); }
+#else
+    explicit PhaseRange(const char*) {}
+#endif
+    PhaseRange(const PhaseRange&) = delete;
+    PhaseRange& operator=(const PhaseRange&) = delete;
+};
+
 struct DevBuf {
     void* p = nullptr;
     size_t cap = 0;
@@ -461,6 +474,7 @@ static o3g_status target_finish(o3g_ctx* c, bool normals_late);
 // stored); the caller runs target_finish after its own work (o3g_set_clouds)
 static o3g_status set_target_impl(o3g_ctx* c, const float* xyz, const float* normals, int64_t n,
                                   double dmax, cudaEvent_t normals_ready, bool defer_final = false) {
+    PhaseRange nvtx_("o3g:set_target (A0-A1 grid build)");
     if (!c) return fail(O3G_ERR_INVALID_ARGUMENT, "ctx is NULL");
     if (!xyz) return fail(O3G_ERR_INVALID_ARGUMENT, "target xyz is required");
     if (n <= 0 || n > 0x7ffffffeLL) return fail(O3G_ERR_INVALID_ARGUMENT, "n_target must be in [1, 2^31-2]");
@@ -624,6 +638,7 @@ static o3g_status set_target_impl(o3g_ctx* c, const float* xyz, const float* nor
 // the end of o3g_set_target: wait for the build, read the occupied-cell count (and the
 // late normals' finiteness flag), then the x-order inside cells for dense targets
 static o3g_status target_finish(o3g_ctx* c, bool normals_late) {
+    PhaseRange nvtx_("o3g:set_target finish");
     const GridDev g = c->g;
     const int64_t n = c->m;
     uint32_t* mm = c->misc.as<uint32_t>();
@@ -680,6 +695,7 @@ static o3g_status source_finish(o3g_ctx* c);
 // defer: enqueue only, on c->exec as the caller set it (no wait for the user stream, no
 // final sync); the caller runs source_finish afterwards (o3g_set_clouds)
 static o3g_status set_source_impl(o3g_ctx* c, const float* xyz, int64_t n, const double order_T[16], bool defer) {
+    PhaseRange nvtx_("o3g:set_source (A2 ordering)");
     if (!c) return fail(O3G_ERR_INVALID_ARGUMENT, "ctx is NULL");
     if (!xyz) return fail(O3G_ERR_INVALID_ARGUMENT, "source xyz is required");
     // (the kernels' 32-bit batch cursors step by up to 2^24 past the last query)
@@ -819,6 +835,7 @@ static o3g_status set_source_impl(o3g_ctx* c, const float* xyz, int64_t n, const
 
 // the end of o3g_set_source: wait, read the finiteness flag and the source bbox
 static o3g_status source_finish(o3g_ctx* c) {
+    PhaseRange nvtx_("o3g:set_source finish");
     const uint32_t* smm = c->misc.as<uint32_t>() + 24;
     int32_t h_bad = 0;
     uint32_t h_mm[6];
@@ -1065,6 +1082,7 @@ static void init_state(o3g_ctx* c, const double* T, int max_it, double ef, doubl
 o3g_status o3g_icp_step(o3g_ctx* c, const double T_in[16], int32_t* corr_out, double JTJ_out[36],
                         double JTr_out[6], double* inlier_count, double* sum_sq_dist,
                         double* terms_out) {
+    PhaseRange nvtx_("o3g:icp_step (A3-A6, A9)");
     if (!c) return fail(O3G_ERR_INVALID_ARGUMENT, "ctx is NULL");
     if (!rigid_ok(T_in)) return fail(O3G_ERR_INVALID_ARGUMENT, "T_in is not a rigid transform");
     if (!c->src_ready) return fail(O3G_ERR_INVALID_ARGUMENT, "o3g_set_target and o3g_set_source must be called first");
@@ -1142,6 +1160,7 @@ static o3g_status run_prologue(o3g_ctx* c, bool certm, bool trace) {
 }
 
 static o3g_status build_graph(o3g_ctx* c, int max_it, int blocks, int sblocks) {
+    PhaseRange nvtx_("o3g:build_graph");
     GraphKey key;
     key.max_it = max_it + 1000000 * c->estimation;
     key.search = c->search;
@@ -1210,6 +1229,7 @@ o3g_status o3g_icp_run(o3g_ctx* c, const double init_T[16], int32_t max_iteratio
                        double relative_fitness, double relative_rmse, double T_out[16],
                        double* fitness, double* inlier_rmse, o3g_icp_info* info,
                        double* hist_fitness, double* hist_rmse) {
+    PhaseRange nvtx_("o3g:icp_run (A3-A8 loop)");
     if (!c) return fail(O3G_ERR_INVALID_ARGUMENT, "ctx is NULL");
     if (!rigid_ok(init_T)) return fail(O3G_ERR_INVALID_ARGUMENT, "init_T is not a rigid transform");
     if (max_iterations < 0 || max_iterations > 100000) return fail(O3G_ERR_INVALID_ARGUMENT, "max_iterations must be in [0, 100000]");
